@@ -1,0 +1,385 @@
+#!/usr/bin/env python
+"""OSCAR hot-path benchmark on B200 (see DESIGN.md §8 for every definition used here).
+
+Workload (N=1, BASELINE.json configs[1], "C2"): Llama-3-8B-shaped GQA decode — 32 q / 8 kv
+heads, d=128, 2-bit codes, G=64, batch 16, 32k context, 32 layers.  One timed STEP = one
+decode step through all 32 layers: quantize_append of the 16 new K/V rows (overwriting slot
+L-1 so the context stays 32768) + attend(q) over the packed paged cache, per layer.  Each
+layer's pool is 335.5 MB (> 126 MB L2) and the 32 pools are visited in turn, so no input is
+L2-resident between uses.  The pools are filled beforehand by our own prefill
+quantize_append (timed: the append half of the metric), with rotations produced by our own
+on-device calibration (timed: C3 per-rank shard).
+
+value = algorithmic bytes of all ranks' timed steps / max-over-ranks device time (GB/s).
+Multi-GPU (torchrun, NCCL): every rank runs the same per-GPU workload (weak scaling); the
+calibration covariances are all-reduced over NCCL (the path's only exchange step).
+`--impl reference`: the CPU oracle timed on bounded samples of the same workload (rank 0).
+"""
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "packed-KV decode attention HBM GB/s (% of 8 TB/s); quantize-append tokens/s"
+NOMINAL_HBM_GBS = 8000.0
+B_, L_, HQ, HKV, D, BITS, G, P = 16, 32768, 32, 8, 128, 2, 64, 64
+TOKHEAD_BYTES = 2 * (D * BITS // 8 + 4 * (D // G))                    # = 80 for b=2, G=64
+APPEND_BYTES_PER_TOKHEAD = 2 * D * 2 + TOKHEAD_BYTES + 8 // HKV       # 593 B
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), float(j.get("bf16_tflops_sustained", 1417.2)), "measured"
+    except Exception:
+        return 6650.0, 1400.0, "fallback"
+
+
+# ------------------------------------------------------------------ clocks sampler (NVML)
+class ClockSampler:
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                bits = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, v in self.REASONS.items():
+                    if bits & k and k != 0x1:
+                        self.reasons.add(v)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        s = sorted(self.samples)
+        return {"sm_mhz": s[len(s) // 2], "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(s)}
+
+
+def cpu_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        n = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+        return int(n)
+    except Exception:
+        return 1
+
+
+# ------------------------------------------------------------------ reference (CPU oracle) arm
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    import numpy as np
+    import oracle as O
+    from paper_2605_17757_b200 import synth
+    rng = np.random.default_rng(1)
+    fmt = O.PageFormat(D, BITS, G, P)
+    max_pages = L_ // P
+    # one (sequence, kv-head) unit per step: 32768 tokens of one KV head, its 4 query heads
+    pool = synth.random_pool(rng, max_pages, 1, fmt.page_bytes, fmt.meta_off, P * (D // G))
+    RK, RV = synth.gen_rotation(rng, 1, D), synth.gen_rotation(rng, 1, D)
+    q = synth.gen_decode_q(rng, 1, HQ // HKV, D)
+    pt = np.arange(max_pages, dtype=np.int32)[None]
+    unit_bytes = L_ * TOKHEAD_BYTES + 2 * (HQ // HKV) * D * 2
+    for _ in range(args.warmup):
+        O.attend(q, pt, [L_], pool, RK, RV, fmt, 1)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        O.attend(q, pt, [L_], pool, RK, RV, fmt, 1)
+    dt = time.perf_counter() - t0
+    gbs = unit_bytes * args.steps / dt / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": workload_config(args),
+        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": cpu_threads(), "kind": "oracle",
+                         "sample": "per step: 1 sequence x 1 kv head (4 q heads) x 32768 tokens "
+                                   "of the C2 decode workload (1/128 of one layer-step)"},
+        "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args):
+    return {"workload": "C2: Llama-3-8B-shaped GQA decode on 1 B200 per rank (BASELINE.json configs[1])",
+            "batch": B_, "context": L_, "q_heads": HQ, "kv_heads": HKV, "head_dim": D, "bits": BITS,
+            "group": G, "page": P, "layers": args.layers, "parallelism": f"weak x{args.gpus} (per-rank C2)",
+            "l2": "inputs larger than L2: 335.5 MB pool per layer, layers visited in turn"}
+
+
+# ------------------------------------------------------------------ GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="oscar", choices=["oscar", "reference"])
+    ap.add_argument("--layers", type=int, default=32)
+    ap.add_argument("--variant", type=int, default=0, help="0 = fastest kernels, 1 = simple reference kernels")
+    ap.add_argument("--no-extras", action="store_true", help="skip calibration / prefill / e2e / cpu legs (ncu runs)")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2605_17757_b200 import binding as Bnd
+    from paper_2605_17757_b200 import synth
+    from paper_2605_17757_b200.parallel import allreduce_covariances, barrier, max_over_ranks
+
+    hbm_peak, _, peak_kind = measured_peaks()
+    o = Bnd.Oscar(Bnd.Config(num_q_heads=HQ, num_kv_heads=HKV, bits=BITS, group_size=G, page_size=P))
+    o.set_variant(args.variant)
+    stream = torch.cuda.current_stream()
+    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+    NL = args.layers
+    max_pages = L_ // P
+    extras = {}
+    launches_per_layer = 4    # append (1) + attend: q_rotate, partial, merge (3)
+
+    # ---------------- calibration: C3 per-rank shard (65536 tokens/layer, NL layers)
+    calib_tokens = 65536
+    RK_all = torch.empty((NL, HKV, D, D), dtype=torch.float32, device=dev)
+    RV_all = torch.empty_like(RK_all)
+    if not args.no_extras:
+        Q = synth.torch_queries(gen, calib_tokens, HQ, HKV, D, dev)
+        SV = synth.torch_sv(gen, calib_tokens, HQ, D, dev)
+        acc = torch.zeros((NL, HKV, 2, D, D), dtype=torch.float64, device=dev)
+        for l in range(2):  # warm
+            o.calib_accumulate(Q, SV, acc[0])
+        acc.zero_()
+        torch.cuda.synchronize(); barrier(world)
+        e0, e1, e2, e3 = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        e0.record()
+        for l in range(NL):
+            o.calib_accumulate(Q, SV, acc[l])
+        e1.record()
+        allreduce_covariances(acc, world)
+        e2.record()
+        info = torch.empty((NL * HKV, 2), dtype=torch.int32, device=dev)
+        o.calib_finalize(acc, NL * HKV, calib_tokens * world * (HQ // HKV), RK_all, RV_all, None, info)
+        e3.record()
+        torch.cuda.synchronize()
+        t_acc, t_ar, t_fin = e0.elapsed_time(e1), e1.elapsed_time(e2), e2.elapsed_time(e3)
+        sweeps = info.cpu().numpy()
+        cov_bytes = NL * 2 * calib_tokens * HQ * D * 2
+        cov_flops = NL * 2 * calib_tokens * HQ * 2 * D * D
+        extras["calibration"] = {
+            "config": f"C3 shard: {calib_tokens} tokens/rank/layer x {NL} layers x {HKV} kv heads, "
+                      f"{world} rank(s), then {NL * HKV * 2} 128x128 eigensolves",
+            "accumulate_ms": t_acc, "accumulate_GBps": cov_bytes / t_acc / 1e6,
+            "accumulate_TFLOPs": cov_flops / t_acc / 1e9,
+            "allreduce_ms": t_ar, "allreduce_bytes": acc.numel() * 8,
+            "finalize_ms": t_fin, "jacobi_sweeps_max": int(sweeps.max()),
+        }
+        del Q, SV, acc
+    else:
+        for l in range(NL):
+            RK_all[l] = synth.torch_rotation(gen, HKV, D, dev)
+            RV_all[l] = synth.torch_rotation(gen, HKV, D, dev)
+
+    # ---------------- prefill: fill NL layer pools with our quantize_append (timed on layer 0)
+    page_bytes = o.page_bytes()
+    pools = [torch.empty((B_ * max_pages, HKV, page_bytes), dtype=torch.uint8, device=dev) for _ in range(NL)]
+    page_table = torch.arange(B_ * max_pages, dtype=torch.int32, device=dev).reshape(B_, max_pages)
+    page_table = page_table.reshape(-1)[torch.randperm(B_ * max_pages, generator=gen, device=dev)].reshape(B_, max_pages).contiguous()
+    pos = torch.arange(L_, device=dev)
+    pre_slots = (page_table[:, pos // P].long() * P + (pos % P)).reshape(-1).contiguous()   # [B*L]
+    Tpre = B_ * L_
+    Kp = synth.torch_keys(gen, Tpre, HKV, D, dev)
+    Vp = synth.torch_values(gen, Tpre, HKV, D, dev)
+    for l in range(NL):
+        o.quantize_append(Kp, Vp, pre_slots, RK_all[l], RV_all[l], pools[l])
+    torch.cuda.synchronize()
+    if not args.no_extras:
+        reps = 5
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier(world)
+        ea.record()
+        for r in range(reps):
+            o.quantize_append(Kp, Vp, pre_slots, RK_all[r % NL], RV_all[r % NL], pools[r % NL])
+        eb.record(); torch.cuda.synchronize()
+        t = ea.elapsed_time(eb) / reps
+        t = max_over_ranks(t, world)
+        ap_bytes = Tpre * HKV * APPEND_BYTES_PER_TOKHEAD
+        extras["append"] = {
+            "config": f"C2 prefill: {Tpre} tokens x {HKV} kv heads into one layer pool (per rank)",
+            "tokens_per_s": Tpre * world / t * 1e3, "token_heads_per_s": Tpre * HKV * world / t * 1e3,
+            "ms": t, "GBps": ap_bytes * world / t / 1e6,
+            "pct_of_8TBps": ap_bytes / t / 1e6 / NOMINAL_HBM_GBS * 100,
+            "roofline": {"bound": "hbm", "achieved": ap_bytes / t / 1e6, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": ap_bytes / t / 1e6 / hbm_peak, "traffic": None,
+                         "algorithmic_bytes_per_launch": ap_bytes, "peak_kind": peak_kind},
+        }
+    del Kp, Vp
+
+    # ---------------- decode step inputs (per layer)
+    qs = [synth.torch_decode_q(gen, B_, HQ, D, dev) for _ in range(NL)]
+    ks = [synth.torch_keys(gen, B_, HKV, D, dev) for _ in range(NL)]
+    vs = [synth.torch_values(gen, B_, HKV, D, dev) for _ in range(NL)]
+    dec_slots = (page_table[:, (L_ - 1) // P].long() * P + (L_ - 1) % P).contiguous()
+    seq_lens = torch.full((B_,), L_, dtype=torch.int32, device=dev)
+    ws = torch.empty(o.attend_workspace_bytes(B_, max_pages), dtype=torch.uint8, device=dev)
+    outs = [torch.empty((B_, HQ, D), dtype=torch.bfloat16, device=dev) for _ in range(NL)]
+
+    attn_bytes = B_ * L_ * HKV * TOKHEAD_BYTES + 2 * B_ * HQ * D * 2
+    app_bytes = B_ * HKV * APPEND_BYTES_PER_TOKHEAD
+    step_bytes = NL * (attn_bytes + app_bytes)
+
+    def layer(l, ev=None):
+        o.quantize_append(ks[l], vs[l], dec_slots, RK_all[l], RV_all[l], pools[l])
+        if ev is not None:
+            ev[0].record()
+        o.attend(qs[l], page_table, seq_lens, pools[l], RK_all[l], RV_all[l], ws, outs[l])
+        if ev is not None:
+            ev[1].record()
+
+    for _ in range(args.warmup):
+        for l in range(NL):
+            layer(l)
+    torch.cuda.synchronize()
+    evs = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(NL)]
+           for _ in range(args.steps)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t_start.record()
+        for s in range(args.steps):
+            for l in range(NL):
+                layer(l, evs[s][l])
+        t_end.record()
+        torch.cuda.synchronize()
+    barrier(world)
+    ms_total = max_over_ranks(t_start.elapsed_time(t_end), world)
+    ms_step = ms_total / args.steps
+    value = step_bytes * world * args.steps / (ms_total * 1e-3) / 1e9
+    attn_ms = float(np.mean([a.elapsed_time(b) for st in evs for (a, b) in st]))
+    attn_gbs = attn_bytes / attn_ms / 1e6
+
+    # ---------------- e2e: host-pinned inputs/outputs through the public API
+    e2e = None
+    if not args.no_extras:
+        hq = [q.cpu().pin_memory() for q in qs]
+        hk = [k.cpu().pin_memory() for k in ks]
+        hv = [v.cpu().pin_memory() for v in vs]
+        ho = [torch.empty((B_, HQ, D), dtype=torch.bfloat16).pin_memory() for _ in range(NL)]
+        dq = [torch.empty_like(q) for q in qs]
+        dk = [torch.empty_like(k) for k in ks]
+        dv = [torch.empty_like(v) for v in vs]
+
+        def e2e_step():
+            for l in range(NL):
+                dq[l].copy_(hq[l], non_blocking=True)
+                dk[l].copy_(hk[l], non_blocking=True)
+                dv[l].copy_(hv[l], non_blocking=True)
+                o.quantize_append(dk[l], dv[l], dec_slots, RK_all[l], RV_all[l], pools[l])
+                o.attend(dq[l], page_table, seq_lens, pools[l], RK_all[l], RV_all[l], ws, outs[l])
+                ho[l].copy_(outs[l], non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize(); barrier(world)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(args.steps):
+            e2e_step()
+        b.record(); torch.cuda.synchronize()
+        ms_e2e = max_over_ranks(a.elapsed_time(b), world)
+        e2e = {"value": step_bytes * world * args.steps / (ms_e2e * 1e-3) / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": NL * (qs[0].numel() + ks[0].numel() + vs[0].numel()) * 2,
+               "d2h_bytes_per_step": NL * outs[0].numel() * 2, "ms_per_step": ms_e2e / args.steps}
+
+    # ---------------- CPU oracle beside the GPU (rank 0, N=1 only, bounded sample)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_extras:
+        import oracle as O
+        fmt = O.PageFormat(D, BITS, G, P)
+        b = 0
+        sub = pools[0][page_table[b].long()].cpu().numpy()
+        qn = qs[0][b:b + 1].float().cpu().numpy()
+        rk, rv = RK_all[0].cpu().numpy(), RV_all[0].cpu().numpy()
+        pt_local = np.arange(max_pages, dtype=np.int32)[None]
+        t0 = time.perf_counter()
+        ref, _ = O.attend(qn, pt_local, [L_], sub, rk, rv, fmt, HKV)
+        dt = time.perf_counter() - t0
+        samp_bytes = L_ * HKV * TOKHEAD_BYTES + 2 * HQ * D * 2
+        got = outs[0][b].float().cpu().numpy()
+        cpu = {"value": samp_bytes / dt / 1e9, "unit": "GB/s", "cores": cpu_threads(), "kind": "oracle",
+               "sample": "layer 0, sequence 0, all 8 kv heads x 32768 tokens (1/16 of one layer-step)",
+               "seconds": dt, "parity_max_abs_vs_gpu_bf16": float(np.abs(got - ref[0]).max())}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u2 codes + f16 meta, f32 accumulate", "data": "synthetic",
+        "config": workload_config(args),
+        "pct_of_8TBps": value / world / NOMINAL_HBM_GBS * 100,
+        "roofline": {"bound": "hbm", "achieved": attn_gbs, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": attn_gbs / hbm_peak, "traffic": None, "kernel": "oscar_attend (q_rotate+partial+merge)",
+                     "algorithmic_bytes_per_launch": attn_bytes, "avg_launch_us": attn_ms * 1e3,
+                     "peak_kind": peak_kind},
+        "gpu_launches": launches_per_layer * NL * args.steps,
+        "clocks": clk.summary(),
+        "variant": args.variant,
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if cpu:
+        line["cpu_baseline"] = cpu
+    line.update(extras)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

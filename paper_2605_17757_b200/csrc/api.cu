@@ -1,0 +1,207 @@
+// C ABI of liboscar.so (include/oscar.h): validation, context, launches on the caller's stream.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "common.cuh"
+
+namespace oscar {
+cudaError_t launch_append_simple(const oscar_ctx& c, int mode, const void* K, const void* V,
+                                 const float* Krot, const float* Vrot, const int64_t* slots,
+                                 int64_t T, const float* RK, const float* RV, void* pool,
+                                 float* rot_out, cudaStream_t s);
+cudaError_t launch_append_tc(const oscar_ctx& c, const void* K, const void* V,
+                             const int64_t* slots, int64_t T, const float* RK, const float* RV,
+                             void* pool, cudaStream_t s);
+bool append_tc_supported(const oscar_ctx& c);
+}  // namespace oscar
+
+namespace {
+thread_local std::string g_last_error;
+
+oscar_status fail(oscar_status st, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+oscar_status fail(oscar_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return st;
+}
+
+oscar_status cuda_status(cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return OSCAR_OK;
+  return fail(OSCAR_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+}  // namespace
+
+extern "C" {
+
+const char* oscar_last_error(void) { return g_last_error.c_str(); }
+const char* oscar_version(void) { return "oscar-b200 0.1.0 (sm_100a)"; }
+
+oscar_status oscar_create(const oscar_config* cfg, oscar_ctx** out) {
+  if (!cfg || !out) return fail(OSCAR_ERR_ARG, "oscar_create: NULL argument");
+  const oscar_config& c = *cfg;
+  if (c.head_dim <= 0 || (c.head_dim & (c.head_dim - 1)))
+    return fail(OSCAR_ERR_DIM, "head_dim %d is not a power of two", c.head_dim);
+  if (c.head_dim != oscar::kD)
+    return fail(OSCAR_ERR_UNSUPPORTED, "this build implements head_dim 128 only (got %d)", c.head_dim);
+  if (c.num_q_heads <= 0 || c.num_kv_heads <= 0 || c.num_q_heads % c.num_kv_heads)
+    return fail(OSCAR_ERR_ARG, "need H_q %% H_kv == 0 and both > 0 (got %d, %d)", c.num_q_heads,
+                c.num_kv_heads);
+  const int g = c.num_q_heads / c.num_kv_heads;
+  if (g > 8) return fail(OSCAR_ERR_UNSUPPORTED, "GQA ratio %d > 8 not implemented", g);
+  if (c.bits != 2 && c.bits != 3 && c.bits != 4)
+    return fail(OSCAR_ERR_ARG, "bits must be 2, 3 or 4 (got %d)", c.bits);
+  if (c.bits == 3) return fail(OSCAR_ERR_UNSUPPORTED, "3-bit codes are not implemented on the GPU path");
+  if (c.group_size != 32 && c.group_size != 64 && c.group_size != 128)
+    return fail(OSCAR_ERR_ARG, "group_size must be 32, 64 or 128 (got %d)", c.group_size);
+  const int P = c.page_size == 0 ? 64 : c.page_size;
+  if (P < 16 || P > 256 || P % 16) return fail(OSCAR_ERR_ARG, "page_size must be a multiple of 16 in [16, 256] (got %d)", P);
+  if (!(c.clip_ratio_k > 0.f && c.clip_ratio_k <= 1.f) || !(c.clip_ratio_v > 0.f && c.clip_ratio_v <= 1.f))
+    return fail(OSCAR_ERR_ARG, "clip ratios must be in (0, 1]");
+  if (c.softmax_scale < 0.f || !std::isfinite(c.softmax_scale))
+    return fail(OSCAR_ERR_ARG, "softmax_scale must be >= 0 and finite");
+  if (c.attend_pages_per_split < 0) return fail(OSCAR_ERR_ARG, "attend_pages_per_split must be >= 0");
+
+  oscar_ctx* x = new (std::nothrow) oscar_ctx();
+  if (!x) return fail(OSCAR_ERR_ARG, "out of host memory");
+  x->cfg = c;
+  x->d = c.head_dim; x->hq = c.num_q_heads; x->hkv = c.num_kv_heads; x->g = g;
+  x->bits = c.bits; x->G = c.group_size; x->P = P; x->ng = x->d / x->G;
+  x->row_bytes = x->d * x->bits / 8;
+  x->vcodes_off = P * x->row_bytes;
+  x->meta_off = 2 * P * x->row_bytes;
+  const int raw = 2 * P * x->row_bytes + P * x->ng * 8;
+  x->page_bytes = (raw + 255) / 256 * 256;
+  auto clip_idx = [&](float rho) {
+    if (rho >= 1.f) return -1;
+    return (int)std::ceil((double)rho * x->d) - 1;
+  };
+  x->clip_k_idx = clip_idx(c.clip_ratio_k);
+  x->clip_v_idx = clip_idx(c.clip_ratio_v);
+  x->scale = c.softmax_scale > 0.f ? c.softmax_scale : 1.f / std::sqrt((float)x->d);
+  x->pages_per_split = c.attend_pages_per_split;
+  x->variant = 0;
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess &&
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    sms = 148;
+  cudaGetLastError();
+  x->num_sms = sms > 0 ? sms : 148;
+  *out = x;
+  return OSCAR_OK;
+}
+
+void oscar_destroy(oscar_ctx* ctx) { delete ctx; }
+
+size_t oscar_page_bytes(const oscar_ctx* ctx) { return ctx ? (size_t)ctx->page_bytes : 0; }
+
+oscar_status oscar_set_variant(oscar_ctx* ctx, int32_t variant) {
+  if (!ctx || variant < 0 || variant > 1) return fail(OSCAR_ERR_ARG, "oscar_set_variant: bad argument");
+  ctx->variant = variant;
+  return OSCAR_OK;
+}
+
+oscar_status oscar_calib_accumulate(const oscar_ctx* ctx, const void* Q, const void* SV,
+                                    int64_t N, double* acc, void* stream) {
+  if (!ctx) return fail(OSCAR_ERR_ARG, "NULL ctx");
+  if (N < 0) return fail(OSCAR_ERR_ARG, "N must be >= 0 (got %lld)", (long long)N);
+  if (N == 0) return OSCAR_OK;
+  if (!Q || !SV || !acc) return fail(OSCAR_ERR_ARG, "oscar_calib_accumulate: NULL pointer");
+  return cuda_status(oscar::launch_cov_accum(*ctx, Q, SV, N, acc, as_stream(stream)), "cov_accum");
+}
+
+oscar_status oscar_calib_finalize(const oscar_ctx* ctx, const double* acc, int32_t n_mats,
+                                  int64_t n_rows, float* R_K, float* R_V, double* evals,
+                                  int32_t* info, void* stream) {
+  if (!ctx) return fail(OSCAR_ERR_ARG, "NULL ctx");
+  if (n_mats <= 0 || n_rows <= 0) return fail(OSCAR_ERR_ARG, "n_mats and n_rows must be > 0 (empty dump)");
+  if (!acc || !R_K || !R_V) return fail(OSCAR_ERR_ARG, "oscar_calib_finalize: NULL pointer");
+  cudaStream_t s = as_stream(stream);
+  oscar_status st = cuda_status(
+      oscar::launch_jacobi_compose(*ctx, acc, n_mats, 1.0 / (double)n_rows, R_K, R_V, evals, info, s),
+      "jacobi_compose");
+  if (st != OSCAR_OK || !info) return st;
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_status(e, "calib_finalize sync");
+  const int n = 2 * n_mats;
+  int32_t* h = new int32_t[n];
+  e = cudaMemcpy(h, info, sizeof(int32_t) * n, cudaMemcpyDeviceToHost);
+  int bad = -1;
+  for (int i = 0; e == cudaSuccess && i < n; ++i)
+    if (h[i] < 0) { bad = i; break; }
+  delete[] h;
+  if (e != cudaSuccess) return cuda_status(e, "calib_finalize info copy");
+  if (bad >= 0) return fail(OSCAR_ERR_CONVERGENCE, "Jacobi did not converge for matrix %d", bad);
+  return OSCAR_OK;
+}
+
+oscar_status oscar_quantize_append(const oscar_ctx* ctx, const void* K, const void* V,
+                                   const int64_t* slots, int64_t T, const float* R_K,
+                                   const float* R_V, void* pool, void* stream) {
+  if (!ctx) return fail(OSCAR_ERR_ARG, "NULL ctx");
+  if (T < 0) return fail(OSCAR_ERR_ARG, "T must be >= 0");
+  if (T == 0) return OSCAR_OK;
+  if (!K || !V || !slots || !R_K || !R_V || !pool) return fail(OSCAR_ERR_ARG, "oscar_quantize_append: NULL pointer");
+  cudaStream_t s = as_stream(stream);
+  if (ctx->variant == 0 && oscar::append_tc_supported(*ctx))
+    return cuda_status(oscar::launch_append_tc(*ctx, K, V, slots, T, R_K, R_V, pool, s), "append_tc");
+  return cuda_status(oscar::launch_append_simple(*ctx, 0, K, V, nullptr, nullptr, slots, T, R_K, R_V,
+                                                 pool, nullptr, s), "append_simple");
+}
+
+oscar_status oscar_rotate(const oscar_ctx* ctx, const void* X, const float* R, float* Xrot,
+                          int64_t T, void* stream) {
+  if (!ctx) return fail(OSCAR_ERR_ARG, "NULL ctx");
+  if (T < 0) return fail(OSCAR_ERR_ARG, "T must be >= 0");
+  if (T == 0) return OSCAR_OK;
+  if (!X || !R || !Xrot) return fail(OSCAR_ERR_ARG, "oscar_rotate: NULL pointer");
+  // the K half of the append kernel (blockIdx.z = 0) with output = fp32 rows
+  return cuda_status(oscar::launch_append_simple(*ctx, 1, X, X, nullptr, nullptr, nullptr, T, R, R,
+                                                 nullptr, Xrot, as_stream(stream)), "rotate");
+}
+
+oscar_status oscar_quantize_rotated(const oscar_ctx* ctx, const float* Krot, const float* Vrot,
+                                    const int64_t* slots, int64_t T, void* pool, void* stream) {
+  if (!ctx) return fail(OSCAR_ERR_ARG, "NULL ctx");
+  if (T < 0) return fail(OSCAR_ERR_ARG, "T must be >= 0");
+  if (T == 0) return OSCAR_OK;
+  if (!Krot || !Vrot || !slots || !pool) return fail(OSCAR_ERR_ARG, "oscar_quantize_rotated: NULL pointer");
+  return cuda_status(oscar::launch_append_simple(*ctx, 2, nullptr, nullptr, Krot, Vrot, slots, T, nullptr,
+                                                 nullptr, pool, nullptr, as_stream(stream)),
+                     "quantize_rotated");
+}
+
+size_t oscar_attend_workspace_bytes(const oscar_ctx* ctx, int32_t B, int32_t max_pages) {
+  if (!ctx || B <= 0 || max_pages <= 0) return 0;
+  return oscar::attend_workspace_bytes(*ctx, B, max_pages);
+}
+
+oscar_status oscar_attend(const oscar_ctx* ctx, const void* q, const int32_t* page_table,
+                          const int32_t* seq_lens, int32_t B, int32_t max_pages,
+                          const void* pool, const float* R_K, const float* R_V,
+                          void* workspace, size_t workspace_bytes, void* out, int32_t out_fp32,
+                          float* lse, void* stream) {
+  if (!ctx) return fail(OSCAR_ERR_ARG, "NULL ctx");
+  if (B < 0 || max_pages < 0) return fail(OSCAR_ERR_ARG, "B and max_pages must be >= 0");
+  if (B == 0) return OSCAR_OK;
+  if (max_pages == 0) return fail(OSCAR_ERR_ARG, "max_pages must be > 0");
+  if (!q || !page_table || !seq_lens || !pool || !R_K || !R_V || !workspace || !out)
+    return fail(OSCAR_ERR_ARG, "oscar_attend: NULL pointer");
+  const size_t need = oscar::attend_workspace_bytes(*ctx, B, max_pages);
+  if (workspace_bytes < need)
+    return fail(OSCAR_ERR_ARG, "workspace too small: %zu < %zu", workspace_bytes, need);
+  return cuda_status(oscar::launch_attend(*ctx, q, page_table, seq_lens, B, max_pages, pool, R_K, R_V,
+                                          workspace, out, out_fp32, lse, as_stream(stream)),
+                     "attend");
+}
+
+}  // extern "C"

@@ -1,0 +1,87 @@
+// quantize_append — Alg. 1 `Prefill` rotate-before-write + `QuantizeAndWrite`
+// (P:L1639-1643); §4 "KV Cache Update".  This file holds the simple reference
+// kernel (variant 1): rotation on CUDA cores in fp32, then clip / min-max / round / pack.
+// The tensor-core kernel (variant 0) lives in append_tc.cu and shares the epilogue below.
+#include "common.cuh"
+#include "append_epilogue.cuh"
+
+namespace oscar {
+
+constexpr int kAppTok = 32;   // tokens per CTA in the simple kernel
+
+// grid (ceil(T / kAppTok), H_kv, 2 [K, V]); 128 threads; dynamic smem = R (64 KB) + 2 tiles.
+// mode 0: bf16 rows + R -> quantize into pool; 1: bf16 rows + R -> fp32 rotated out;
+// mode 2: fp32 rotated rows -> quantize into pool.
+__global__ void __launch_bounds__(128) append_simple_kernel(
+    int mode, const uint16_t* __restrict__ K, const uint16_t* __restrict__ V,
+    const float* __restrict__ Krot, const float* __restrict__ Vrot,
+    const int64_t* __restrict__ slots, int64_t T, const float* __restrict__ RK,
+    const float* __restrict__ RV, uint8_t* __restrict__ pool, float* __restrict__ rot_out,
+    EpiParams ep) {
+  extern __shared__ __align__(16) float sm[];
+  float* Rs = sm;                       // [128][128]
+  float* xs = sm + kD * kD;             // [kAppTok][128]
+  float* ys = xs + kAppTok * kD;        // [kAppTok][128]
+  const int h = blockIdx.y, isV = blockIdx.z;
+  const int64_t t0 = (int64_t)blockIdx.x * kAppTok;
+  const int nt = (int)((T - t0) < (int64_t)kAppTok ? (T - t0) : (int64_t)kAppTok);
+  const int tid = threadIdx.x;
+
+  if (mode != 2) {
+    const float* R = (isV ? RV : RK) + (size_t)h * kD * kD;
+    for (int e = tid; e < kD * kD / 4; e += 128)
+      reinterpret_cast<float4*>(Rs)[e] = reinterpret_cast<const float4*>(R)[e];
+    const uint16_t* X = isV ? V : K;
+    for (int e = tid; e < kAppTok * kD; e += 128) {
+      const int r = e / kD, c = e % kD;
+      xs[e] = (r < nt) ? bf16_to_f32(X[((t0 + r) * ep.hkv + h) * kD + c]) : 0.f;
+    }
+    __syncthreads();
+    float acc[kAppTok];
+#pragma unroll
+    for (int r = 0; r < kAppTok; ++r) acc[r] = 0.f;
+    for (int k = 0; k < kD; ++k) {
+      const float rk = Rs[k * kD + tid];
+#pragma unroll
+      for (int r = 0; r < kAppTok; ++r) acc[r] = fmaf(xs[r * kD + k], rk, acc[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < kAppTok; ++r) ys[r * kD + tid] = acc[r];
+    if (mode == 1) {
+      for (int r = 0; r < nt; ++r)
+        rot_out[((t0 + r) * ep.hkv + h) * kD + tid] = acc[r];
+      return;
+    }
+  } else {
+    const float* X = isV ? Vrot : Krot;
+    for (int e = tid; e < kAppTok * kD; e += 128) {
+      const int r = e / kD, c = e % kD;
+      ys[e] = (r < nt) ? X[((t0 + r) * ep.hkv + h) * kD + c] : 0.f;
+    }
+  }
+  __syncthreads();
+  // epilogue: warp w handles rows w, w+4, ...; lane owns channels 4*lane .. 4*lane+3
+  const int warp = tid >> 5, lane = tid & 31;
+  for (int r = warp; r < nt; r += 4) {
+    const float4 y4 = *reinterpret_cast<const float4*>(&ys[r * kD + 4 * lane]);
+    float y[4] = {y4.x, y4.y, y4.z, y4.w};
+    quantize_store_row_warp(ep, y, lane, slots[t0 + r], h, isV, pool);
+  }
+}
+
+cudaError_t launch_append_simple(const oscar_ctx& c, int mode, const void* K, const void* V,
+                                 const float* Krot, const float* Vrot, const int64_t* slots,
+                                 int64_t T, const float* RK, const float* RV, void* pool,
+                                 float* rot_out, cudaStream_t s) {
+  const int smem = (kD * kD + 2 * kAppTok * kD) * (int)sizeof(float);
+  cudaError_t e = cudaFuncSetAttribute(append_simple_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  dim3 grid((unsigned)((T + kAppTok - 1) / kAppTok), c.hkv, 2);
+  append_simple_kernel<<<grid, 128, smem, s>>>(
+      mode, static_cast<const uint16_t*>(K), static_cast<const uint16_t*>(V), Krot, Vrot, slots,
+      T, RK, RV, static_cast<uint8_t*>(pool), rot_out, make_epi_params(c));
+  return cudaGetLastError();
+}
+
+}  // namespace oscar

@@ -1,0 +1,109 @@
+// Clip + per-group min-max quantize + pack + store of one rotated row (App A.5, P:L1235-1311;
+// Alg. 1 QuantizeAndWrite P:L1639-1643).  Operation order = reading Z4:
+//   s = (mx - mn) / q_max [fp32 RN]; s16 = fp16_rn(s); m16 = fp16_rn(mn);
+//   inv = s16 > 0 ? 1 / float(s16) : 0; t = (x - float(m16)) * inv [RN, RN, no FMA];
+//   c = clamp(rint(t), 0, q_max).
+#pragma once
+#include "common.cuh"
+
+namespace oscar {
+
+struct EpiParams {
+  int hkv, P, page_bytes, row_bytes, vcodes_off, meta_off, ng, G, bits;
+  int clip_k_idx, clip_v_idx;
+};
+
+inline EpiParams make_epi_params(const oscar_ctx& c) {
+  EpiParams e;
+  e.hkv = c.hkv; e.P = c.P; e.page_bytes = c.page_bytes; e.row_bytes = c.row_bytes;
+  e.vcodes_off = c.vcodes_off; e.meta_off = c.meta_off; e.ng = c.ng; e.G = c.G; e.bits = c.bits;
+  e.clip_k_idx = c.clip_k_idx; e.clip_v_idx = c.clip_v_idx;
+  return e;
+}
+
+// Quantize one group given its min / max; returns the codes of x[0..n) and the metadata.
+__device__ __forceinline__ void minmax_params(float mn, float mx, float qmax, __half& s16,
+                                              __half& m16, float& m, float& inv) {
+  const float s = __fdiv_rn(__fsub_rn(mx, mn), qmax);
+  s16 = __float2half_rn(s);
+  m16 = __float2half_rn(mn);
+  const float sf = __half2float(s16);
+  m = __half2float(m16);
+  inv = sf > 0.f ? __fdiv_rn(1.f, sf) : 0.f;
+}
+
+__device__ __forceinline__ int quant_code(float x, float m, float inv, int qmax) {
+  const float t = __fmul_rn(__fsub_rn(x, m), inv);
+  return min(max(__float2int_rn(t), 0), qmax);
+}
+
+// Nearest-rank clip threshold over a 128-value row held 4 per lane (reading Z6):
+// tau = the value v with #{|x| < v} <= k < #{|x| <= v}.
+__device__ __forceinline__ float warp_row_rank_select(const float a[4], int k) {
+  int less[4] = {0, 0, 0, 0}, le[4] = {0, 0, 0, 0};
+  for (int src = 0; src < 32; ++src) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float o = __shfl_sync(0xffffffffu, a[q], src);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) { less[i] += (o < a[i]); le[i] += (o <= a[i]); }
+    }
+  }
+  float tau = -1.f;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    if (less[i] <= k && k < le[i]) tau = a[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) tau = fmaxf(tau, __shfl_xor_sync(0xffffffffu, tau, o));
+  return tau;
+}
+
+// One warp owns one row: lane holds channels 4*lane .. 4*lane+3 in y[] (bits in {2, 4}).
+__device__ __forceinline__ void quantize_store_row_warp(const EpiParams& ep, float y[4], int lane,
+                                                        int64_t slot, int h, int isV,
+                                                        uint8_t* __restrict__ pool) {
+  const int cidx = isV ? ep.clip_v_idx : ep.clip_k_idx;
+  if (cidx >= 0) {
+    const float a[4] = {fabsf(y[0]), fabsf(y[1]), fabsf(y[2]), fabsf(y[3])};
+    const float tau = warp_row_rank_select(a, cidx);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) y[i] = fminf(fmaxf(y[i], -tau), tau);
+  }
+  float mn = fminf(fminf(y[0], y[1]), fminf(y[2], y[3]));
+  float mx = fmaxf(fmaxf(y[0], y[1]), fmaxf(y[2], y[3]));
+  const int lanes_per_group = ep.G / 4;
+  for (int o = 1; o < lanes_per_group; o <<= 1) {
+    mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  const int qmax = (1 << ep.bits) - 1;
+  __half s16, m16;
+  float m, inv;
+  minmax_params(mn, mx, (float)qmax, s16, m16, m, inv);
+  int c[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) c[i] = quant_code(y[i], m, inv, qmax);
+
+  const int64_t page = slot / ep.P;
+  const int off = (int)(slot % ep.P);
+  uint8_t* blk = pool + (page * ep.hkv + h) * (int64_t)ep.page_bytes;
+  const int nbytes = ep.bits / 2;            // bytes per lane-chunk (4 codes)
+  const uint32_t chunk = ep.bits == 2
+      ? (uint32_t)(c[0] | (c[1] << 2) | (c[2] << 4) | (c[3] << 6))
+      : (uint32_t)(c[0] | (c[1] << 4) | (c[2] << 8) | (c[3] << 12));
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    if (k >= nbytes) break;
+    const int j = lane * nbytes + k;         // byte index inside the row
+    const uint8_t v = (uint8_t)(chunk >> (8 * k));
+    if (!isV) blk[off * ep.row_bytes + j] = v;
+    else blk[ep.vcodes_off + (off >> 2) * 4 * ep.row_bytes + 4 * j + (off & 3)] = v;
+  }
+  if ((lane % lanes_per_group) == 0) {
+    const int grp = lane / lanes_per_group;
+    const __half2 sm = __halves2half2(s16, m16);
+    *reinterpret_cast<__half2*>(blk + ep.meta_off + (off * ep.ng + grp) * 8 + (isV ? 4 : 0)) = sm;
+  }
+}
+
+}  // namespace oscar

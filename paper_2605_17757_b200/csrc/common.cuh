@@ -1,0 +1,50 @@
+// Shared internals of liboscar.so (CUDA, sm_100a).  Not part of the ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cstdint>
+
+#include "oscar.h"
+
+struct oscar_ctx {
+  oscar_config cfg;
+  int d, hq, hkv, g, bits, G, P, ng;     // ng = d / G groups per row
+  int row_bytes;                          // d * bits / 8
+  int vcodes_off, meta_off, page_bytes;   // FORMAT offsets inside one (page, head) block
+  int clip_k_idx, clip_v_idx;             // nearest-rank index ceil(rho*d)-1, or -1 = off
+  float scale;                            // softmax scale (1/sqrt(d) by default)
+  int pages_per_split;                    // 0 = auto
+  int variant;                            // 0 = fastest, 1 = simple reference kernels
+  int num_sms;
+};
+
+namespace oscar {
+
+constexpr int kD = 128;                   // head_dim implemented by this build
+constexpr float kLog2e = 1.4426950408889634f;
+
+// ---------------------------------------------------------------- launch declarations
+// calib.cu
+cudaError_t launch_cov_accum(const oscar_ctx& c, const void* Q, const void* SV, int64_t N,
+                             double* acc, cudaStream_t s);
+cudaError_t launch_jacobi_compose(const oscar_ctx& c, const double* acc, int n_mats,
+                                  double inv_rows, float* RK, float* RV, double* evals,
+                                  int32_t* info, cudaStream_t s);
+// attend.cu
+size_t attend_workspace_bytes(const oscar_ctx& c, int B, int max_pages);
+cudaError_t launch_attend(const oscar_ctx& c, const void* q, const int32_t* page_table,
+                          const int32_t* seq_lens, int B, int max_pages, const void* pool,
+                          const float* RK, const float* RV, void* ws, void* out, int out_fp32,
+                          float* lse, cudaStream_t s);
+
+// ---------------------------------------------------------------- device helpers
+__device__ __forceinline__ float bf16_to_f32(uint16_t b) {
+  return __uint_as_float(static_cast<uint32_t>(b) << 16);
+}
+
+__device__ __forceinline__ int plan_splits(int max_pages, int pps) {
+  return (max_pages + pps - 1) / pps;
+}
+
+}  // namespace oscar

@@ -1,0 +1,295 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded
+inputs.  Tolerances (north star):
+  * rotated values: per row max|Δ| / ‖x̃‖₂ <= 1e-5                     (reading Z26)
+  * codes / metadata / pool bytes: bit-exact given identical rotated inputs
+  * full append: bit-exact except rounding-boundary flips (|Δcode| = 1 where the oracle's
+    pre-round value is within 1e-4 of a .5 boundary, or fp16 metadata 1 ulp apart)
+  * attention: fp32-output mode <= 2e-3 max-abs vs the fp64 oracle; bf16 mode ==
+    RNE(fp32 mode) bit-for-bit (reading Z25)
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2605_17757_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def T(x, dtype=None):
+    torch = _torch()
+    t = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    return t.to(dtype) if dtype is not None else t
+
+
+def make(**kw):
+    from paper_2605_17757_b200 import binding as B
+    return B.Oscar(B.Config(**kw))
+
+
+# ---------------------------------------------------------------------------- rotation
+@pytest.mark.parametrize("T_", [1, 33, 300])
+def test_rotate_parity(T_):
+    torch = _torch()
+    rng = np.random.default_rng(100 + T_)
+    H = 3
+    X = synth.gen_keys(rng, T_, H, 128)
+    R = synth.gen_rotation(rng, H, 128)
+    o = make(num_q_heads=H, num_kv_heads=H)
+    out = torch.empty((T_, H, 128), dtype=torch.float32, device="cuda")
+    o.rotate(T(X, torch.bfloat16), T(R), out)
+    ref = O.rotate(X, R).astype(np.float64)
+    got = out.cpu().numpy().astype(np.float64)
+    err = np.abs(got - ref).max(axis=-1) / np.linalg.norm(ref, axis=-1)
+    assert err.max() <= 1e-5, err.max()
+
+
+# ---------------------------------------------------------------------------- quantizer
+def _adversarial_rows(rng, n, H):
+    X = rng.standard_normal((n, H, 128)).astype(np.float32) * rng.uniform(0.01, 30, (n, H, 1)).astype(np.float32)
+    X[0] = 0.0                                       # zero rows: s16 = 0
+    X[1, :, :64] = 3.25                              # constant group
+    X[2] *= 1e-7                                     # s underflows fp16 -> s16 = 0 / subnormal
+    X[3] = np.round(X[3] * 2) / 2                    # many exact half-steps
+    X[4, :, ::2] = 7.0; X[4, :, 1::2] = -7.0         # two-valued groups
+    return X
+
+
+@pytest.mark.parametrize("bits,G,rho", [(2, 64, (1.0, 1.0)), (2, 32, (0.96, 0.92)),
+                                        (4, 32, (1.0, 1.0)), (4, 128, (0.96, 0.92)),
+                                        (2, 128, (0.5, 0.999))])
+def test_quantize_rotated_bit_exact(bits, G, rho):
+    torch = _torch()
+    rng = np.random.default_rng(bits * 1000 + G)
+    H, Tn, npages = 2, 333, 8
+    fmt = O.PageFormat(128, bits, G, 64)
+    Kr = _adversarial_rows(rng, Tn, H)
+    Vr = _adversarial_rows(rng, Tn, H)[::-1].copy()
+    slots = rng.permutation(npages * 64)[:Tn].astype(np.int64)
+    ref = np.zeros((npages, H, fmt.page_bytes), np.uint8)
+    O.quantize_rotated(Kr, Vr, slots, fmt, ref, rho[0], rho[1])
+    o = make(num_q_heads=H, num_kv_heads=H, bits=bits, group_size=G, clip_ratio_k=rho[0],
+             clip_ratio_v=rho[1])
+    pool = torch.zeros((npages, H, o.page_bytes()), dtype=torch.uint8, device="cuda")
+    o.quantize_rotated(T(Kr), T(Vr), T(slots), pool)
+    got = pool.cpu().numpy()
+    diff = np.argwhere(got != ref)
+    assert diff.size == 0, f"{len(diff)} bytes differ, first {diff[:5]}"
+
+
+# ---------------------------------------------------------------------------- full append
+def _decode_pool(pool, slots, H, fmt):
+    out = []
+    for h in range(H):
+        Kh, Vh = O.read_rows(pool, slots, h, fmt)
+        out.append((Kh, Vh))
+    return out
+
+
+@pytest.mark.parametrize("bits,G,rho,variant", [(2, 64, (1.0, 1.0), 0), (4, 32, (0.96, 0.92), 0),
+                                                (2, 64, (1.0, 1.0), 1)])
+def test_quantize_append_parity(bits, G, rho, variant):
+    torch = _torch()
+    rng = np.random.default_rng(7 + bits + G)
+    H, Tn, npages = 8, 1000, 20
+    fmt = O.PageFormat(128, bits, G, 64)
+    K = synth.gen_keys(rng, Tn, H, 128)
+    V = synth.gen_values(rng, Tn, H, 128)
+    RK, RV = synth.gen_rotation(rng, H, 128), synth.gen_rotation(rng, H, 128)
+    slots = rng.permutation(npages * 64)[:Tn].astype(np.int64)
+    ref = np.zeros((npages, H, fmt.page_bytes), np.uint8)
+    O.quantize_append(K, V, slots, RK, RV, fmt, ref, rho[0], rho[1])
+    o = make(num_q_heads=H * 4, num_kv_heads=H, bits=bits, group_size=G, clip_ratio_k=rho[0],
+             clip_ratio_v=rho[1])
+    o.set_variant(variant)
+    pool = torch.zeros((npages, H, o.page_bytes()), dtype=torch.uint8, device="cuda")
+    o.quantize_append(T(K, torch.bfloat16), T(V, torch.bfloat16), T(slots), T(RK), T(RV), pool)
+    got = pool.cpu().numpy()
+    nbad = int((got != ref).sum())
+    frac = nbad / got.size
+    # bytes differ only at rounding-boundary flips; dequantized rows agree within one step
+    assert frac < 2e-4, frac
+    rot = {"K": O.rotate(K, RK), "V": O.rotate(V, RV)}
+    for h, ((Kg, Vg), (Ko, Vo)) in enumerate(zip(_decode_pool(got, slots, H, fmt), _decode_pool(ref, slots, H, fmt))):
+        for name, g_, r_ in [("K", Kg, Ko), ("V", Vg, Vo)]:
+            x = rot[name][:, h].astype(np.float64)
+            step = np.abs(x).max() / 2 ** bits * 4
+            assert np.abs(g_ - r_).max() <= step, (name, h)
+
+
+# ---------------------------------------------------------------------------- attention
+def _oracle_pool(rng, fmt, B, Hkv, L, shuffle=True):
+    max_pages = (max(L) + fmt.P - 1) // fmt.P if len(L) else 1
+    max_pages = max(max_pages, 1)
+    pt = synth.contiguous_page_table(B, max_pages, shuffle_rng=rng if shuffle else None)
+    pool = np.zeros((B * max_pages, Hkv, fmt.page_bytes), np.uint8)
+    RK, RV = synth.gen_rotation(rng, Hkv, 128), synth.gen_rotation(rng, Hkv, 128)
+    for b in range(B):
+        if L[b] == 0:
+            continue
+        K = synth.gen_keys(rng, L[b], Hkv, 128)
+        V = synth.gen_values(rng, L[b], Hkv, 128)
+        slots = synth.slots_for(pt[b:b + 1], np.arange(L[b])[None], fmt.P).reshape(-1)
+        O.quantize_append(K, V, slots, RK, RV, fmt, pool)
+    return pt, pool, RK, RV
+
+
+def _run_attend(o, q, pt, L, pool, RK, RV):
+    torch = _torch()
+    B, Hq, _ = q.shape
+    ws = torch.empty(o.attend_workspace_bytes(B, pt.shape[1]), dtype=torch.uint8, device="cuda")
+    out32 = torch.empty((B, Hq, 128), dtype=torch.float32, device="cuda")
+    out16 = torch.empty((B, Hq, 128), dtype=torch.bfloat16, device="cuda")
+    lse = torch.empty((B, Hq), dtype=torch.float32, device="cuda")
+    args = (T(q, torch.bfloat16), T(pt), T(np.asarray(L, np.int32)), T(pool), T(RK), T(RV), ws)
+    o.attend(*args, out32, lse)
+    o.attend(*args, out16)
+    torch.cuda.synchronize()
+    return out32, out16, lse
+
+
+@pytest.mark.parametrize("cfg", [
+    dict(name="C1", Hq=1, Hkv=1, bits=4, G=32, B=64, L="ramp256"),
+    dict(name="C2small", Hq=32, Hkv=8, bits=2, G=64, B=3, L=[1000, 77, 0]),
+    dict(name="g8", Hq=16, Hkv=2, bits=2, G=128, B=2, L=[513, 64]),
+    dict(name="g2b4", Hq=4, Hkv=2, bits=4, G=64, B=2, L=[300, 1]),
+])
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("pps", [0, 1, 3])
+def test_attend_parity(cfg, variant, pps):
+    torch = _torch()
+    rng = np.random.default_rng(hash(cfg["name"]) % 2 ** 31)
+    fmt = O.PageFormat(128, cfg["bits"], cfg["G"], 64)
+    L = list(range(4, 260, 4)) if cfg["L"] == "ramp256" else cfg["L"]
+    B = cfg["B"]
+    pt, pool, RK, RV = _oracle_pool(rng, fmt, B, cfg["Hkv"], L)
+    q = synth.gen_decode_q(rng, B, cfg["Hq"], 128)
+    ref, ref_lse = O.attend(q, pt, L, pool, RK, RV, fmt, cfg["Hkv"])
+    o = make(num_q_heads=cfg["Hq"], num_kv_heads=cfg["Hkv"], bits=cfg["bits"], group_size=cfg["G"],
+             attend_pages_per_split=pps)
+    o.set_variant(variant)
+    out32, out16, lse = _run_attend(o, q, pt, L, pool, RK, RV)
+    got = out32.cpu().numpy().astype(np.float64)
+    err = np.abs(got - ref).max()
+    assert err <= 2e-3, err
+    assert torch.equal(out32.to(torch.bfloat16).view(torch.int16), out16.view(torch.int16))
+    lg = lse.cpu().numpy()
+    fin = np.isfinite(ref_lse)
+    assert np.array_equal(np.isfinite(lg), fin)
+    assert np.abs(lg[fin] - ref_lse[fin]).max() <= 1e-3
+
+
+def test_attend_page_indirection_invariance():
+    """Shuffling the physical pages (same logical cache) must not change the output."""
+    torch = _torch()
+    rng = np.random.default_rng(5)
+    fmt = O.PageFormat(128, 2, 64, 64)
+    pt, pool, RK, RV = _oracle_pool(rng, fmt, 2, 8, [700, 450], shuffle=False)
+    q = synth.gen_decode_q(rng, 2, 32, 128)
+    o = make()
+    a, _, _ = _run_attend(o, q, pt, [700, 450], pool, RK, RV)
+    perm = rng.permutation(pool.shape[0])
+    pool2 = np.empty_like(pool)
+    pool2[perm] = pool
+    pt2 = perm[pt].astype(np.int32)
+    b, _, _ = _run_attend(o, q, pt2, [700, 450], pool2, RK, RV)
+    assert torch.equal(a, b)
+
+
+def test_attend_full_size_sampled():
+    """C2 at full size (B=16, L=32768, 32q/8kv, 2-bit, G=64) in the bench's launch
+    configuration, on a synthetic random packed pool; two sequences checked against the
+    oracle (all 32 heads each)."""
+    torch = _torch()
+    B, L, Hq, Hkv, P = 16, 32768, 32, 8, 64
+    o = make(num_q_heads=Hq, num_kv_heads=Hkv, bits=2, group_size=64)
+    fmt = O.PageFormat(128, 2, 64, P)
+    max_pages = L // P
+    gen = torch.Generator(device="cuda").manual_seed(1)
+    pool = synth.torch_random_pool(gen, B * max_pages, Hkv, o.page_bytes(), fmt.meta_off, P * 2, "cuda")
+    rng = np.random.default_rng(1)
+    pt = synth.contiguous_page_table(B, max_pages, shuffle_rng=rng)
+    RK, RV = synth.gen_rotation(rng, Hkv, 128), synth.gen_rotation(rng, Hkv, 128)
+    q = synth.gen_decode_q(rng, B, Hq, 128)
+    seq = np.full(B, L, np.int32)
+    seq[5] = L - 1000
+    ws = torch.empty(o.attend_workspace_bytes(B, max_pages), dtype=torch.uint8, device="cuda")
+    out = torch.empty((B, Hq, 128), dtype=torch.float32, device="cuda")
+    o.attend(T(q, torch.bfloat16), T(pt), T(seq), pool, T(RK), T(RV), ws, out)
+    got = out.cpu().numpy()
+    for b in [0, 5]:
+        sub = pool[torch.from_numpy(pt[b].astype(np.int64)).cuda()].cpu().numpy()
+        ref, _ = O.attend(q[b:b + 1], np.arange(max_pages, dtype=np.int32)[None], [seq[b]], sub, RK, RV,
+                          fmt, Hkv)
+        assert np.abs(got[b] - ref[0]).max() <= 2e-3
+
+
+# ---------------------------------------------------------------------------- calibration
+def test_calibration_parity_by_invariants():
+    torch = _torch()
+    rng = np.random.default_rng(21)
+    N, Hq, Hkv = 3000, 8, 2
+    Q = synth.gen_queries(rng, N, Hq, Hkv, 128)
+    SV = synth.gen_sv(rng, N, Hq, 128)
+    o = make(num_q_heads=Hq, num_kv_heads=Hkv)
+    acc = torch.zeros((Hkv, 2, 128, 128), dtype=torch.float64, device="cuda")
+    o.calib_accumulate(T(Q[:1234], torch.bfloat16), T(SV[:1234], torch.bfloat16), acc)
+    o.calib_accumulate(T(Q[1234:], torch.bfloat16), T(SV[1234:], torch.bfloat16), acc)
+    ref = np.stack([O.cov_accumulate(Q, Hkv), O.cov_accumulate(SV, Hkv)], axis=1)
+    got = acc.cpu().numpy()
+    for h in range(Hkv):
+        for w in range(2):
+            assert np.linalg.norm(got[h, w] - ref[h, w]) / np.linalg.norm(ref[h, w]) <= 1e-5
+    RK = torch.empty((Hkv, 128, 128), dtype=torch.float32, device="cuda")
+    RV = torch.empty_like(RK)
+    ev = torch.empty((Hkv, 2, 128), dtype=torch.float64, device="cuda")
+    info = torch.empty((Hkv, 2), dtype=torch.int32, device="cuda")
+    n_rows = N * (Hq // Hkv)
+    o.calib_finalize(acc, Hkv, n_rows, RK, RV, ev, info)
+    assert (info.cpu().numpy() > 0).all()
+    H = O.hadamard(128)
+    Pbr = H.T @ O.compose_rotation(np.eye(128))
+    for h in range(Hkv):
+        for w, R in enumerate([RK[h].cpu().numpy().astype(np.float64), RV[h].cpu().numpy().astype(np.float64)]):
+            C = ref[h, w] / n_rows
+            lam_o, U_o = O.eigh_desc(C)
+            lam_g = ev[h, w].cpu().numpy()
+            assert np.abs(R.T @ R - np.eye(128)).max() <= 1e-5                       # orthogonal
+            d = np.diag(R.T @ C @ R)
+            assert np.abs(d / (np.trace(C) / 128) - 1).max() <= 1e-5                  # Lemma
+            U = R @ Pbr.T @ H.T                                                       # undo H P_br
+            assert np.linalg.norm(C @ U - U * lam_g) / np.linalg.norm(C) <= 1e-5    # residual
+            dC = np.linalg.norm(got[h, w] / n_rows - C, 2)
+            assert np.abs(lam_g - lam_o).max() <= dC + 1e-6 * lam_o[0]                # Weyl
+            gaps = np.minimum(np.abs(np.diff(lam_o, prepend=np.inf)), np.abs(np.diff(lam_o, append=-np.inf)))
+            ok = gaps / lam_o[0] > 1e-3
+            dots = np.abs(np.sum(U[:, ok] * U_o[:, ok], axis=0))
+            assert (1 - dots).max() <= 1e-4                                           # Davis-Kahan
+            assert np.all(np.diff(lam_g) <= 0)
+
+
+def test_calibration_on_worked_example_spectrum():
+    torch = _torch()
+    rng = np.random.default_rng(4)
+    lam = np.concatenate([[162.5, 85.5, 35.6, 17.4, 11.6, 7.5, 6.1, 5.0],
+                          np.geomspace(4.9, 0.25, 112), [0.24, 0.22, 0.22, 0.20, 0.18, 0.05, 0.027, 0.009]])
+    W = synth.haar(rng, 128)
+    C = W @ np.diag(lam) @ W.T
+    acc = torch.from_numpy(np.stack([C, C])[None]).cuda()
+    o = make(num_q_heads=1, num_kv_heads=1)
+    RK = torch.empty((1, 128, 128), dtype=torch.float32, device="cuda")
+    RV = torch.empty_like(RK)
+    ev = torch.empty((1, 2, 128), dtype=torch.float64, device="cuda")
+    info = torch.empty((1, 2), dtype=torch.int32, device="cuda")
+    o.calib_finalize(acc, 1, 1, RK, RV, ev, info)
+    np.testing.assert_allclose(ev[0, 0].cpu().numpy(), np.sort(lam)[::-1], rtol=1e-9, atol=1e-12)
+    R = RK[0].cpu().numpy().astype(np.float64)
+    dg = np.diag(R.T @ C @ R)
+    assert abs(dg.max() / dg.mean() - 1.0) < 1e-5                                     # 1.00

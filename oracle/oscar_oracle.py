@@ -252,11 +252,15 @@ def unpack_codes(packed: np.ndarray, bits: int, d: int) -> np.ndarray:
 
 # ----------------------------------------------------------------------------------
 # Paged cache format (reading Z24, DESIGN.md §5 "FORMAT"): pool[num_pages][H_kv][page_bytes];
-# slot = page·P + offset.  One (page, kv-head) block =
-#   K codes  [P][d·b/8]  ‖  V codes [P/4][d·b/8][4]  ‖  meta [P][d/G][4] fp16 (s_K, m_K, s_V, m_V)
-# padded to a multiple of 256 bytes.  K rows are stored as written (row r at r·d·b/8).
-# V rows are byte-interleaved in groups of 4 tokens: byte j of row r lives at
-# (r//4)·4·(d·b/8) + 4·j + r%4.  The row bitstream itself (reading Z22) is unchanged.
+# slot = page·P + offset u (P a multiple of 16).  One (page, kv-head) block =
+#   K codes [P rows of rb = d·b/8 bytes] ‖ V codes [P·rb bytes] ‖ meta [P·(d/G)·8 bytes]
+# padded to a multiple of 256 bytes.  The row bitstream (reading Z22) is unchanged; only
+# the placement of whole rows / bytes inside the block is permuted for the decode kernel:
+#   K row u   -> row position 16·(u//16) + 8·(u%2) + (u%16)//2   (even tokens of each
+#                16-token tile first)
+#   V byte j of row u -> (u//4)·4·rb + 4·pos(j) + u%4, pos(j) = (rb/8)·(j%8) + j//8
+#                (4-token groups, byte-interleaved, words permuted)
+#   meta (s_K, m_K, s_V, m_V) fp16 of (u, group γ) -> (u//4)·32·(d/G) + 32·γ + 8·(u%4)
 # ----------------------------------------------------------------------------------
 @dataclass(frozen=True)
 class PageFormat:
@@ -286,10 +290,20 @@ class PageFormat:
         raw = 2 * self.P * self.row_bytes + self.P * (self.d // self.G) * 8
         return (raw + 255) // 256 * 256
 
-    def vbyte_offsets(self, off: int) -> np.ndarray:
-        """Offsets (within the block) of the row_bytes bytes of V row `off`."""
-        j = np.arange(self.row_bytes)
-        return self.vcodes_off + (off // 4) * 4 * self.row_bytes + 4 * j + off % 4
+    def krow_offset(self, u: int) -> int:
+        """Offset (within the block) of K row u."""
+        return self.kcodes_off + (16 * (u // 16) + 8 * (u % 2) + (u % 16) // 2) * self.row_bytes
+
+    def vbyte_offsets(self, u: int) -> np.ndarray:
+        """Offsets (within the block) of the row_bytes bytes of V row u."""
+        rb = self.row_bytes
+        j = np.arange(rb)
+        pos = (rb // 8) * (j % 8) + j // 8
+        return self.vcodes_off + (u // 4) * 4 * rb + 4 * pos + u % 4
+
+    def meta_offset(self, u: int, grp: int) -> int:
+        ng = self.d // self.G
+        return self.meta_off + (u // 4) * 32 * ng + 32 * grp + 8 * (u % 4)
 
 
 def quantize_rotated(Kr, Vr, slots, fmt: PageFormat, pool: np.ndarray, rho_k=1.0, rho_v=1.0):
@@ -307,11 +321,13 @@ def quantize_rotated(Kr, Vr, slots, fmt: PageFormat, pool: np.ndarray, rho_k=1.0
         for h in range(H):
             blk = pool[page, h]
             rb = fmt.row_bytes
-            blk[fmt.kcodes_off + off * rb: fmt.kcodes_off + (off + 1) * rb] = pk[t, h]
+            ko = fmt.krow_offset(off)
+            blk[ko: ko + rb] = pk[t, h]
             blk[fmt.vbyte_offsets(off)] = pv[t, h]
-            meta = np.stack([sk[t, h], mk[t, h], sv[t, h], mv[t, h]], axis=-1).astype(np.float16)
-            mb = meta.reshape(-1).view(np.uint8)
-            blk[fmt.meta_off + off * ng * 8: fmt.meta_off + (off + 1) * ng * 8] = mb
+            for grp in range(ng):
+                meta = np.array([sk[t, h, grp], mk[t, h, grp], sv[t, h, grp], mv[t, h, grp]], np.float16)
+                mo = fmt.meta_offset(off, grp)
+                blk[mo: mo + 8] = meta.view(np.uint8)
     return pool
 
 
@@ -332,9 +348,12 @@ def read_rows(pool: np.ndarray, slots, head: int, fmt: PageFormat):
     for t in range(T):
         page, off = divmod(int(slots[t]), fmt.P)
         blk = pool[page, head]
-        pk[t] = blk[fmt.kcodes_off + off * rb: fmt.kcodes_off + (off + 1) * rb]
+        ko = fmt.krow_offset(off)
+        pk[t] = blk[ko: ko + rb]
         pv[t] = blk[fmt.vbyte_offsets(off)]
-        meta[t] = blk[fmt.meta_off + off * ng * 8: fmt.meta_off + (off + 1) * ng * 8]
+        for grp in range(ng):
+            mo = fmt.meta_offset(off, grp)
+            meta[t, grp * 8: grp * 8 + 8] = blk[mo: mo + 8]
     m = meta.view(np.float16).reshape(T, ng, 4)
     Kh = dequantize_rows(unpack_codes(pk, fmt.bits, fmt.d), m[..., 0], m[..., 1], fmt.G)
     Vh = dequantize_rows(unpack_codes(pv, fmt.bits, fmt.d), m[..., 2], m[..., 3], fmt.G)

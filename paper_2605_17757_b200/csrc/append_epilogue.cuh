@@ -96,13 +96,13 @@ __device__ __forceinline__ void quantize_store_row_warp(const EpiParams& ep, flo
     if (k >= nbytes) break;
     const int j = lane * nbytes + k;         // byte index inside the row
     const uint8_t v = (uint8_t)(chunk >> (8 * k));
-    if (!isV) blk[off * ep.row_bytes + j] = v;
-    else blk[ep.vcodes_off + (off >> 2) * 4 * ep.row_bytes + 4 * j + (off & 3)] = v;
+    if (!isV) blk[fmt_krow(off) * ep.row_bytes + j] = v;
+    else blk[ep.vcodes_off + fmt_vbyte(off, j, ep.row_bytes)] = v;
   }
   if ((lane % lanes_per_group) == 0) {
     const int grp = lane / lanes_per_group;
     const __half2 sm = __halves2half2(s16, m16);
-    *reinterpret_cast<__half2*>(blk + ep.meta_off + (off * ep.ng + grp) * 8 + (isV ? 4 : 0)) = sm;
+    *reinterpret_cast<__half2*>(blk + ep.meta_off + fmt_meta(off, grp, ep.ng) + (isV ? 4 : 0)) = sm;
   }
 }
 

@@ -72,23 +72,23 @@ __global__ void __launch_bounds__(128) attend_partial_simple(AttnParams p) {
     for (int e = tid; e < p.page_bytes / 16; e += 128) reinterpret_cast<uint4*>(pg)[e] = src[e];
     __syncthreads();
     const int valid = min(P, seq_len - pi * P);
-    const __half* meta = reinterpret_cast<const __half*>(pg + p.meta_off);
+    const uint8_t* meta = pg + p.meta_off;
     // scores
     for (int e = tid; e < g * P; e += 128) {
       const int i = e / P, t = e % P;
       float s = -INFINITY;
       if (t < valid) {
         s = 0.f;
+        const uint8_t* krow = pg + fmt_krow(t) * rb;
         for (int grp = 0; grp < p.ng; ++grp) {
           float dot = 0.f;
           for (int c = grp * p.G; c < (grp + 1) * p.G; ++c) {
             const int bit = c * p.bits;
-            const int code = (pg[t * rb + (bit >> 3)] >> (bit & 7)) & qmax;
+            const int code = (krow[bit >> 3] >> (bit & 7)) & qmax;
             dot = fmaf(qs[i * kD + c], (float)code, dot);
           }
-          const float sk = __half2float(meta[(t * p.ng + grp) * 4 + 0]);
-          const float mk = __half2float(meta[(t * p.ng + grp) * 4 + 1]);
-          s += sk * dot + mk * qsum[i * 8 + grp];
+          const __half* mt = reinterpret_cast<const __half*>(meta + fmt_meta(t, grp, p.ng));
+          s += __half2float(mt[0]) * dot + __half2float(mt[1]) * qsum[i * 8 + grp];
         }
       }
       sc[i * P + t] = s;
@@ -127,10 +127,9 @@ __global__ void __launch_bounds__(128) attend_partial_simple(AttnParams p) {
       const int jb = bit >> 3, sh = bit & 7;
       for (int i = 0; i < g; ++i) acc[i] *= alpha[i];
       for (int t = 0; t < valid; ++t) {
-        const int code = (pg[p.vcodes_off + (t >> 2) * 4 * rb + 4 * jb + (t & 3)] >> sh) & qmax;
-        const float sv = __half2float(meta[(t * p.ng + grp) * 4 + 2]);
-        const float mv = __half2float(meta[(t * p.ng + grp) * 4 + 3]);
-        const float v = fmaf(sv, (float)code, mv);
+        const int code = (pg[p.vcodes_off + fmt_vbyte(t, jb, rb)] >> sh) & qmax;
+        const __half* mt = reinterpret_cast<const __half*>(meta + fmt_meta(t, grp, p.ng));
+        const float v = fmaf(__half2float(mt[2]), (float)code, __half2float(mt[3]));
         for (int i = 0; i < g; ++i) acc[i] = fmaf(sc[i * P + t], v, acc[i]);
       }
     }

@@ -43,8 +43,21 @@ __device__ __forceinline__ float bf16_to_f32(uint16_t b) {
   return __uint_as_float(static_cast<uint32_t>(b) << 16);
 }
 
-__device__ __forceinline__ int plan_splits(int max_pages, int pps) {
-  return (max_pages + pps - 1) / pps;
+// ---------------------------------------------------------------- packed page FORMAT
+// (include/oscar.h).  Placement of rows / bytes inside one (page, head) block:
+//   K row u        -> row position fmt_krow(u) (even tokens of each 16-token tile first)
+//   V byte j of u  -> vcodes_off + fmt_vbyte(u, j, rb) (4-token groups, byte-interleaved,
+//                     word j stored at position (rb/8)(j%8) + j/8)
+//   meta (u, grp)  -> meta_off + fmt_meta(u, grp, ng): 8 B {s_K, m_K, s_V, m_V} fp16
+__host__ __device__ __forceinline__ int fmt_krow(int u) {
+  return 16 * (u >> 4) + 8 * (u & 1) + ((u & 15) >> 1);
+}
+__host__ __device__ __forceinline__ int fmt_vpos(int j, int rb) { return (rb >> 3) * (j & 7) + (j >> 3); }
+__host__ __device__ __forceinline__ int fmt_vbyte(int u, int j, int rb) {
+  return (u >> 2) * 4 * rb + 4 * fmt_vpos(j, rb) + (u & 3);
+}
+__host__ __device__ __forceinline__ int fmt_meta(int u, int grp, int ng) {
+  return (u >> 2) * 32 * ng + 32 * grp + 8 * (u & 3);
 }
 
 }  // namespace oscar

@@ -411,12 +411,20 @@ def test_page_format_and_paged_roundtrip():
             np.testing.assert_array_equal(Kh, O.dequantize_rows(c, s, m, G))
             c, s, m = O.quantize_rows(Vr[:, h], bits, G)
             np.testing.assert_array_equal(Vh, O.dequantize_rows(c, s, m, G))
-        # the first V row's bytes are interleaved with stride 4 (FORMAT)
+        # FORMAT placement: V bytes of a row are interleaved with stride 4 inside its 4-token
+        # group, word order permuted; K rows of a 16-token tile are stored even-tokens-first
         page, off = divmod(int(slots[0]), 64)
+        rb = fmt.row_bytes
         c, _, _ = O.quantize_rows(Vr[:1, 0], bits, G)
         packed = O.pack_codes(c, bits)[0]
-        base = fmt.vcodes_off + (off // 4) * 4 * fmt.row_bytes + off % 4
-        assert np.array_equal(pool[page, 0, base: base + 4 * fmt.row_bytes: 4], packed)
+        grp_base = fmt.vcodes_off + (off // 4) * 4 * rb + off % 4
+        inv = np.zeros(rb, np.int64)
+        for j in range(rb):
+            inv[(rb // 8) * (j % 8) + j // 8] = j
+        assert np.array_equal(pool[page, 0, grp_base: grp_base + 4 * rb: 4], packed[inv])
+        c, _, _ = O.quantize_rows(Kr[:1, 0], bits, G)
+        kpos = 16 * (off // 16) + 8 * (off % 2) + (off % 16) // 2
+        assert np.array_equal(pool[page, 0, kpos * rb: (kpos + 1) * rb], O.pack_codes(c, bits)[0])
 
 
 def test_paged_attend_matches_rows_and_alg1():

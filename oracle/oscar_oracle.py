@@ -258,9 +258,12 @@ def unpack_codes(packed: np.ndarray, bits: int, d: int) -> np.ndarray:
 # the placement of whole rows / bytes inside the block is permuted for the decode kernel:
 #   K row u   -> row position 16·(u//16) + 8·(u%2) + (u%16)//2   (even tokens of each
 #                16-token tile first)
-#   V byte j of row u -> (u//4)·4·rb + 4·pos(j) + u%4, pos(j) = (rb/8)·(j%8) + j//8
-#                (4-token groups, byte-interleaved, words permuted)
-#   meta (s_K, m_K, s_V, m_V) fp16 of (u, group γ) -> (u//4)·32·(d/G) + 32·γ + 8·(u%4)
+#   V byte j of row u -> 16·rb·(u//16) + 16·(32·(k//4) + 4·(j%8) + (u//4)%4) + 4·(k%4) + u%4
+#                with k = j//8 (one 32-bit word = byte j of 4 consecutive tokens; words
+#                grouped in 16-byte chunks so that the decode kernel's loads are
+#                bank-conflict free)
+#   meta of (u, group γ): chunk c = 128·(d/G)·(u//16) + 128·γ + 32·((u//4)%4);
+#                fp16 (s_K, m_K) at c + 4·(u%4), fp16 (s_V, m_V) at c + 16 + 4·(u%4)
 # ----------------------------------------------------------------------------------
 @dataclass(frozen=True)
 class PageFormat:
@@ -298,12 +301,19 @@ class PageFormat:
         """Offsets (within the block) of the row_bytes bytes of V row u."""
         rb = self.row_bytes
         j = np.arange(rb)
-        pos = (rb // 8) * (j % 8) + j // 8
-        return self.vcodes_off + (u // 4) * 4 * rb + 4 * pos + u % 4
+        k = j // 8
+        lane = 4 * (j % 8) + (u // 4) % 4
+        if (rb // 8) % 4 == 0:      # b in {2, 4}: words in 16-byte chunks per lane
+            word = 128 * (k // 4) + 4 * lane + k % 4
+        else:                       # b = 3: one word per lane
+            word = 32 * k + lane
+        return self.vcodes_off + 16 * rb * (u // 16) + 4 * word + u % 4
 
-    def meta_offset(self, u: int, grp: int) -> int:
+    def meta_offsets(self, u: int, grp: int):
+        """Offsets of the fp16 pairs (s_K, m_K) and (s_V, m_V) of (row u, group grp)."""
         ng = self.d // self.G
-        return self.meta_off + (u // 4) * 32 * ng + 32 * grp + 8 * (u % 4)
+        c = self.meta_off + 128 * ng * (u // 16) + 128 * grp + 32 * ((u // 4) % 4)
+        return c + 4 * (u % 4), c + 16 + 4 * (u % 4)
 
 
 def quantize_rotated(Kr, Vr, slots, fmt: PageFormat, pool: np.ndarray, rho_k=1.0, rho_v=1.0):
@@ -325,9 +335,9 @@ def quantize_rotated(Kr, Vr, slots, fmt: PageFormat, pool: np.ndarray, rho_k=1.0
             blk[ko: ko + rb] = pk[t, h]
             blk[fmt.vbyte_offsets(off)] = pv[t, h]
             for grp in range(ng):
-                meta = np.array([sk[t, h, grp], mk[t, h, grp], sv[t, h, grp], mv[t, h, grp]], np.float16)
-                mo = fmt.meta_offset(off, grp)
-                blk[mo: mo + 8] = meta.view(np.uint8)
+                ko_, vo_ = fmt.meta_offsets(off, grp)
+                blk[ko_: ko_ + 4] = np.array([sk[t, h, grp], mk[t, h, grp]], np.float16).view(np.uint8)
+                blk[vo_: vo_ + 4] = np.array([sv[t, h, grp], mv[t, h, grp]], np.float16).view(np.uint8)
     return pool
 
 
@@ -352,8 +362,9 @@ def read_rows(pool: np.ndarray, slots, head: int, fmt: PageFormat):
         pk[t] = blk[ko: ko + rb]
         pv[t] = blk[fmt.vbyte_offsets(off)]
         for grp in range(ng):
-            mo = fmt.meta_offset(off, grp)
-            meta[t, grp * 8: grp * 8 + 8] = blk[mo: mo + 8]
+            ko_, vo_ = fmt.meta_offsets(off, grp)
+            meta[t, grp * 8: grp * 8 + 4] = blk[ko_: ko_ + 4]
+            meta[t, grp * 8 + 4: grp * 8 + 8] = blk[vo_: vo_ + 4]
     m = meta.view(np.float16).reshape(T, ng, 4)
     Kh = dequantize_rows(unpack_codes(pk, fmt.bits, fmt.d), m[..., 0], m[..., 1], fmt.G)
     Vh = dequantize_rows(unpack_codes(pv, fmt.bits, fmt.d), m[..., 2], m[..., 3], fmt.G)

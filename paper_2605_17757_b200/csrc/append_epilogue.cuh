@@ -102,7 +102,7 @@ __device__ __forceinline__ void quantize_store_row_warp(const EpiParams& ep, flo
   if ((lane % lanes_per_group) == 0) {
     const int grp = lane / lanes_per_group;
     const __half2 sm = __halves2half2(s16, m16);
-    *reinterpret_cast<__half2*>(blk + ep.meta_off + fmt_meta(off, grp, ep.ng) + (isV ? 4 : 0)) = sm;
+    *reinterpret_cast<__half2*>(blk + ep.meta_off + fmt_meta(off, grp, ep.ng) + (isV ? 16 : 0)) = sm;
   }
 }
 

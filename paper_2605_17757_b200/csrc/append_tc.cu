@@ -1,15 +1,338 @@
-// Tensor-core quantize_append (variant 0) — see DESIGN.md §7.
+// Tensor-core quantize_append (variant 0).  Alg. 1 `Prefill` rotate-before-
+// write + `QuantizeAndWrite`; §4 "KV Cache Update".
+//
+// Persistent CTA per (kv head, K|V) "pair" slice, 10 warps:
+//   warp 0      TMA producer: 128-token x 128-channel bf16 tiles of K (or V) for one head,
+//               two 64-channel SWIZZLE_128B boxes per tile, 3-stage smem ring
+//   warp 1      TMEM allocator (256 columns = 2 fp32 accumulators) + single-thread tcgen05.mma
+//               issuer: x̃ = [x x]·[R_hi; R_lo] as 16 UMMA 128x128x16 (bf16 -> fp32 TMEM).  The
+//               bf16 hi/lo split of the fp32 R keeps rotated values within 1e-5 of the fp64
+//               product; R_hi, R_lo stay resident in smem (K-major SW128).
+//   warps 2-9   epilogue: tcgen05.ld 32x32b (thread = token row, 64 channels each), per-group
+//               min/max, fp16 (s, m), codes with the reading-Z4 fp32 operation order, pack, and
+//               store into the slot's page block (FORMAT, common.cuh).
+// Scope of this kernel: b in {2, 4}, G in {32, 64}, no clipping; other configs use the simple
+// kernel (append.cu).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "common.cuh"
 
 namespace oscar {
 
-bool append_tc_supported(const oscar_ctx& c) { (void)c; return false; }
+namespace {
 
-cudaError_t launch_append_tc(const oscar_ctx& c, const void* K, const void* V,
-                             const int64_t* slots, int64_t T, const float* RK, const float* RV,
-                             void* pool, cudaStream_t s) {
-  (void)c; (void)K; (void)V; (void)slots; (void)T; (void)RK; (void)RV; (void)pool; (void)s;
-  return cudaErrorNotSupported;
+constexpr int kTok = 128;          // tokens per tile (UMMA M)
+constexpr int kStages = 3;
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = 64 + 32 * kEpiWarps;
+constexpr int kTileBytes = kTok * kD * 2;       // 32 KB bf16 tile
+constexpr int kBBytes = kD * kD * 2;            // 32 KB bf16 R part
+
+struct TcSmem {
+  alignas(1024) uint8_t Bhi[kBBytes];           // [2 k-chunks][128 rows n][128 B], SW128
+  alignas(1024) uint8_t Blo[kBBytes];
+  alignas(1024) uint8_t A[kStages][kTileBytes]; // [stage][2 k-chunks][128 rows tok][128 B]
+  uint64_t full[kStages], empty[kStages], tfull[2], tempty[2];
+  uint32_t tmem_base;
+};
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(b)), "r"(n));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nW_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra W_%=;\n}\n" ::"r"(su32(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n"
+      ::"r"(su32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(su32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+
+// UMMA shared-memory descriptor, K-major SWIZZLE_128B (8-row x 128-B atoms, SBO = 1024 B)
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+// instruction descriptor: kind::f16, A = B = BF16, D = F32, both K-major, M = 128, N = 128
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
+
+__device__ __forceinline__ void umma(uint32_t dt, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n"
+      ::"r"(dt), "l"(a), "l"(b), "r"(kIdesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(su32(bar))
+               : "memory");
+}
+
+#define OSCAR_LD32(base, v)                                                                          \
+  asm volatile(                                                                                       \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15," \
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"                    \
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),           \
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),       \
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]),    \
+        "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]),    \
+        "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])                                             \
+      : "r"(base))
+
+struct TcParams {
+  const int64_t* slots;
+  int64_t T;
+  const float* RK;
+  const float* RV;
+  uint8_t* pool;
+  int hkv, P, page_bytes, row_bytes, vcodes_off, meta_off, ng, G, bits;
+  int cpp, tiles_per_pair;
+};
+
+}  // namespace
+
+template <int BITS, int G>
+__global__ void __launch_bounds__(kThreads, 1)
+append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant__ CUtensorMap mapV, TcParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  TcSmem& S = *reinterpret_cast<TcSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int pair = blockIdx.x / p.cpp, sub = blockIdx.x % p.cpp;
+  const int h = pair >> 1, isV = pair & 1;
+  const int ntiles = sub < p.tiles_per_pair ? (p.tiles_per_pair - sub + p.cpp - 1) / p.cpp : 0;
+
+  // ---- R -> bf16 hi/lo, transposed to K-major (row n = output channel, k contiguous), SW128
+  {
+    const float* R = (isV ? p.RV : p.RK) + (size_t)h * kD * kD;
+    for (int idx = threadIdx.x; idx < kD * 16; idx += kThreads) {
+      const int n = idx & 127, kc16 = idx >> 7;            // 16 chunks of 8 k
+      uint32_t hi[4], lo[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float r0 = R[(size_t)(8 * kc16 + 2 * e) * kD + n];
+        const float r1 = R[(size_t)(8 * kc16 + 2 * e + 1) * kD + n];
+        const __nv_bfloat16 h0 = __float2bfloat16_rn(r0), h1 = __float2bfloat16_rn(r1);
+        const __nv_bfloat16 l0 = __float2bfloat16_rn(r0 - __bfloat162float(h0));
+        const __nv_bfloat16 l1 = __float2bfloat16_rn(r1 - __bfloat162float(h1));
+        hi[e] = (uint32_t)__bfloat16_as_ushort(h0) | ((uint32_t)__bfloat16_as_ushort(h1) << 16);
+        lo[e] = (uint32_t)__bfloat16_as_ushort(l0) | ((uint32_t)__bfloat16_as_ushort(l1) << 16);
+      }
+      const int kchunk = kc16 >> 3, c16 = kc16 & 7;
+      const int off = kchunk * (kD * 128) + n * 128 + ((c16 ^ (n & 7)) << 4);
+      *reinterpret_cast<uint4*>(S.Bhi + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+      *reinterpret_cast<uint4*>(S.Blo + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+    }
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) { mbar_init(&S.full[s], 1); mbar_init(&S.empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&S.tfull[a], 1); mbar_init(&S.tempty[a], kEpiWarps); }
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;\n" ::"r"(su32(&S.tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // B writes -> async proxy
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = S.tmem_base;
+
+  if (warp == 0) {
+    // ================= TMA producer
+    if (lane == 0) {
+      const CUtensorMap* map = isV ? &mapV : &mapK;
+      for (int i = 0; i < ntiles; ++i) {
+        const int s = i % kStages;
+        mbar_wait(&S.empty[s], ((i / kStages) & 1) ^ 1);
+        mbar_expect_tx(&S.full[s], kTileBytes);
+        const int tok0 = (sub + i * p.cpp) * kTok;
+        tma_load_3d(S.A[s], map, 0, h, tok0, &S.full[s]);
+        tma_load_3d(S.A[s] + kTileBytes / 2, map, 64, h, tok0, &S.full[s]);
+      }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer
+    for (int i = 0; i < ntiles; ++i) {
+      const int s = i % kStages, a = i & 1;
+      mbar_wait(&S.tempty[a], ((i >> 1) & 1) ^ 1);
+      mbar_wait(&S.full[s], (i / kStages) & 1);
+      fence_after();
+      if (lane == 0) {
+        const uint32_t dt = tmem + a * 128;
+        const uint32_t abase = su32(S.A[s]), bh = su32(S.Bhi), bl = su32(S.Blo);
+#pragma unroll
+        for (int part = 0; part < 2; ++part) {
+          const uint32_t bbase = part ? bl : bh;
+#pragma unroll
+          for (int kc = 0; kc < 2; ++kc)
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              const uint32_t ko = kc * (kTileBytes / 2) + kk * 32;
+              umma(dt, sw128_desc(abase + ko), sw128_desc(bbase + kc * (kBBytes / 2) + kk * 32),
+                   (part | kc | kk) != 0);
+            }
+        }
+        umma_commit(&S.empty[s]);     // smem stage free once these MMAs complete
+        umma_commit(&S.tfull[a]);     // accumulator ready for the epilogue
+      }
+      __syncwarp();
+    }
+  } else {
+    // ================= epilogue: thread = token row, 64 channels (half of the row)
+    const int ew = warp - 2;
+    const int quarter = warp & 3;                 // TMEM lane quarter this warp may access
+    const int half = ew >> 2;                     // channels [64·half, 64·half + 64)
+    const int r = quarter * 32 + lane;            // row (token) within the tile
+    constexpr int QMAX = (1 << BITS) - 1;
+    constexpr int GPH = 64 / G;                   // groups in this half
+    for (int i = 0; i < ntiles; ++i) {
+      const int a = i & 1;
+      mbar_wait(&S.tfull[a], (i >> 1) & 1);
+      fence_after();
+      uint32_t v[64];
+      const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + a * 128 + half * 64;
+      OSCAR_LD32(taddr, v);
+      OSCAR_LD32(taddr + 32, (v + 32));
+      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.tempty[a]);
+
+      const int64_t tok = (int64_t)(sub + i * p.cpp) * kTok + r;
+      if (tok >= p.T) continue;
+      const int64_t slot = p.slots[tok];
+      const int64_t page = slot / p.P;
+      const int u = (int)(slot % p.P);
+      uint8_t* blk = p.pool + (page * p.hkv + h) * (int64_t)p.page_bytes;
+      uint32_t packed[BITS * 2];                  // 64 codes · BITS bits = BITS·2 words
+#pragma unroll
+      for (int w = 0; w < BITS * 2; ++w) packed[w] = 0;
+#pragma unroll
+      for (int gi = 0; gi < GPH; ++gi) {
+        float mn = __uint_as_float(v[gi * G]), mx = mn;
+#pragma unroll
+        for (int c = 1; c < G; ++c) {
+          const float x = __uint_as_float(v[gi * G + c]);
+          mn = fminf(mn, x);
+          mx = fmaxf(mx, x);
+        }
+        const float s = __fdiv_rn(__fsub_rn(mx, mn), (float)QMAX);
+        const __half s16 = __float2half_rn(s), m16 = __float2half_rn(mn);
+        const float sf = __half2float(s16), m = __half2float(m16);
+        const float inv = sf > 0.f ? __fdiv_rn(1.f, sf) : 0.f;
+#pragma unroll
+        for (int c = 0; c < G; ++c) {
+          // t = (x - m)·inv (RN, RN), rint via the 1.5·2^23 magic add (round-half-even),
+          // clamp on the float bits (same exponent), low bits = code
+          const float tq = __fadd_rn(__fmul_rn(__fsub_rn(__uint_as_float(v[gi * G + c]), m), inv), 12582912.f);
+          const int bits = min(max(__float_as_int(tq), 0x4B400000), 0x4B400000 + QMAX);
+          const int idx = gi * G + c;             // code index within the half row
+          packed[idx * BITS / 32] |= (uint32_t)(bits & QMAX) << ((idx * BITS) & 31);
+        }
+        const int grp = (half * 64 + gi * G) / G;
+        *reinterpret_cast<__half2*>(blk + p.meta_off + fmt_meta(u, grp, p.ng) + (isV ? 16 : 0)) =
+            __halves2half2(s16, m16);
+      }
+      constexpr int HB = 8 * BITS;                // bytes of this half row
+      if (!isV) {
+        uint8_t* dst = blk + fmt_krow(u) * p.row_bytes + half * HB;
+#pragma unroll
+        for (int w4 = 0; w4 < BITS / 2; ++w4)
+          *reinterpret_cast<uint4*>(dst + 16 * w4) =
+              make_uint4(packed[4 * w4], packed[4 * w4 + 1], packed[4 * w4 + 2], packed[4 * w4 + 3]);
+      } else {
+        uint8_t* vb = blk + p.vcodes_off;
+#pragma unroll
+        for (int jb = 0; jb < HB; ++jb)
+          vb[fmt_vbyte(u, half * HB + jb, p.row_bytes)] = (uint8_t)(packed[jb >> 2] >> (8 * (jb & 3)));
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;\n" ::"r"(tmem));
+  }
+}
+
+// ---------------------------------------------------------------- host side
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+bool make_map(CUtensorMap* m, const void* base, int64_t T, int hkv) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)kD, (cuuint64_t)hkv, (cuuint64_t)T};
+  cuuint64_t strides[2] = {(cuuint64_t)kD * 2, (cuuint64_t)hkv * kD * 2};
+  cuuint32_t box[3] = {64, 1, (cuuint32_t)kTok};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+using TcFn = void (*)(CUtensorMap, CUtensorMap, TcParams);
+TcFn pick(int bits, int G) {
+  if (bits == 2 && G == 64) return append_tc_kernel<2, 64>;
+  if (bits == 2 && G == 32) return append_tc_kernel<2, 32>;
+  if (bits == 4 && G == 64) return append_tc_kernel<4, 64>;
+  if (bits == 4 && G == 32) return append_tc_kernel<4, 32>;
+  return nullptr;
+}
+}  // namespace
+
+bool append_tc_supported(const oscar_ctx& c) {
+  return c.d == 128 && c.clip_k_idx < 0 && c.clip_v_idx < 0 && pick(c.bits, c.G) != nullptr &&
+         encode_fn() != nullptr;
+}
+
+cudaError_t launch_append_tc(const oscar_ctx& c, const void* K, const void* V, const int64_t* slots,
+                             int64_t T, const float* RK, const float* RV, void* pool, cudaStream_t s) {
+  TcFn fn = pick(c.bits, c.G);
+  if (!fn) return cudaErrorNotSupported;
+  if ((reinterpret_cast<uintptr_t>(K) | reinterpret_cast<uintptr_t>(V)) & 15) return cudaErrorMisalignedAddress;
+  CUtensorMap mk, mv;
+  if (!make_map(&mk, K, T, c.hkv) || !make_map(&mv, V, T, c.hkv)) return cudaErrorInvalidValue;
+  TcParams p{};
+  p.slots = slots; p.T = T; p.RK = RK; p.RV = RV; p.pool = static_cast<uint8_t*>(pool);
+  p.hkv = c.hkv; p.P = c.P; p.page_bytes = c.page_bytes; p.row_bytes = c.row_bytes;
+  p.vcodes_off = c.vcodes_off; p.meta_off = c.meta_off; p.ng = c.ng; p.G = c.G; p.bits = c.bits;
+  const int pairs = 2 * c.hkv;
+  p.tiles_per_pair = (int)((T + kTok - 1) / kTok);
+  int cpp = c.num_sms / pairs;
+  if (cpp < 1) cpp = 1;
+  if (cpp > p.tiles_per_pair) cpp = p.tiles_per_pair;
+  p.cpp = cpp;
+  const int smem = (int)sizeof(TcSmem) + 1024;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  fn<<<pairs * cpp, kThreads, smem, s>>>(mk, mv, p);
+  return cudaGetLastError();
 }
 
 }  // namespace oscar

@@ -7,7 +7,7 @@ namespace oscar {
 struct AttnParams {
   int hq, hkv, g, P, bits, G, ng;
   int row_bytes, vcodes_off, meta_off, page_bytes;
-  int max_pages, pps, n_splits;
+  int max_pages, pps, n_splits, batch;
   const int32_t* page_table;   // [B][max_pages]
   const int32_t* seq_lens;     // [B]
   const uint8_t* pool;
@@ -15,8 +15,23 @@ struct AttnParams {
   float* ws_o;                 // [B][H_q][n_splits][128] unnormalized partial õ
   float* ws_m;                 // [B][H_q][n_splits] running max (log2 domain)
   float* ws_l;                 // [B][H_q][n_splits] running sum
+  int16_t* qint;               // [B][H_q][128] round(q̃ / qscale), |.| <= 32639 (IMMA path)
+  float* qscale;               // [B][H_q] max|q̃| / 32639
+  int32_t* qsum;               // [B][H_q][8] Σ_{c in group} qint
+  uint32_t* qfrag;             // [B][H_kv][NT*16][32] IMMA A fragments (hi/lo int8 of qint)
+  int32_t* work;               // work-item counter of the persistent partial kernel
+  int nt;                      // ceil(g * ng / 8)
+  int n_items;                 // B * H_kv * n_splits
 };
 
 bool attend_mma_supported(const oscar_ctx& c);
+
+// IMMA QK k-slot -> channel map (see attend_mma.cu): in K-step kk (0..3), lane t's B
+// registers hold channels 32t .. 32t+31 of the token row; slot = 4t + m (+16 for b1).
+__host__ __device__ __forceinline__ int qk_channel(int bits, int kk, int slot) {
+  const int t = (slot & 15) >> 2, m = slot & 3, hi = slot >> 4;
+  if (bits == 2) return 32 * t + 16 * hi + 4 * m + kk;
+  return 32 * t + 16 * hi + 8 * (kk >> 1) + 2 * m + (kk & 1);
+}
 
 }  // namespace oscar

@@ -1,13 +1,472 @@
-// Tensor-core split-K decode attention (variant 0) — see DESIGN.md §7.
+// Tensor-core split-K decode attention over the packed cache (variant 0).
+// Paper: Alg. 1 DecodeStep attention in the rotated frame; §4 "Decoding
+// Attention Kernel" (unpack bytes, apply the stored scale/zero, accumulate in
+// floating point; split-K partials merged with online softmax by attend_merge_kernel).
+//
+// Persistent, warp-granular: every warp is an independent worker that pulls work items
+// (sequence b, kv head h, split of `pps` pages) from an atomic counter and streams the
+// items' 5120-B page blocks through a private smem ring with cp.async.bulk + mbarrier
+// (evict-first L2 policy; the next item's first pages are prefetched while the current one
+// finishes).  Per page, in chunks of up to 64 tokens:
+//   QK  : IMMA m16n8k32 s8 x u8 -> s32.  A = q̃ quantized to 15 bits and split hi/lo int8
+//         (rows = (hi|lo) x (group, head) "combos", zero outside the combo's group; built once
+//         per (b, h) by q_rotate_kernel), B = the raw 2/4-bit codes expanded to bytes with one
+//         SHF + LOP3 per 4 codes.  Exact integer dots per (token, head, group); the fp32
+//         epilogue applies s_K, m_K (x̂ = s·c + m).
+//   soft: online softmax in the log2 domain, one max per 64-token chunk, lazy (+8) rescale.
+//   PV  : HMMA m16n8k16 f16 -> f32.  A = V codes transposed (channels x tokens): the codes are
+//         masked straight into the fp16 mantissa (subnormal c·2^(b·q)·2^-24, exact), one LOP3
+//         per 2 codes, and each accumulator row is rescaled by 2^(24-b·q) at the end;
+//         B = p·s_V per (token, combo) column; the m_V term is a rank-1 FFMA sum.
+#include <type_traits>
+
 #include "attend_common.cuh"
 
 namespace oscar {
 
-bool attend_mma_supported(const oscar_ctx& c) { (void)c; return false; }
+namespace {
 
-cudaError_t launch_attend_mma(const AttnParams& p, cudaStream_t s) {
-  (void)p; (void)s;
-  return cudaErrorNotSupported;
+constexpr int kWarps = 4;
+
+__device__ __forceinline__ void imma16832(int (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k32.row.col.s32.s8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ void hmma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
+  __half2 h = __floats2half2_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                          uint64_t policy) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+// PV M-tile row -> channel: row gid of M-tile i (+64 for rows gid+8); CPB codes per byte
+template <int BITS>
+__device__ __forceinline__ int pv_channel(int i, int gid, int upper) {
+  constexpr int CPB = 8 / BITS;
+  return CPB * gid + 8 * CPB * (i / CPB) + (i % CPB) + (upper ? 64 : 0);
+}
+
+struct Item {
+  int b, h, split, page0, np, seq_len;
+};
+
+__device__ __forceinline__ Item decode_item(const AttnParams& p, int it) {
+  Item I;
+  I.split = it % p.n_splits;
+  const int bh = it / p.n_splits;
+  I.h = bh % p.hkv;
+  I.b = bh / p.hkv;
+  I.seq_len = p.seq_lens[I.b];
+  I.page0 = I.split * p.pps;
+  const int npg = (I.seq_len + p.P - 1) / p.P;
+  I.np = max(0, min(p.pps, npg - I.page0));
+  return I;
+}
+
+}  // namespace
+
+template <int BITS, int GQ, int NG>
+__global__ void __launch_bounds__(kWarps * 32) attend_partial_mma(AttnParams p, int S) {
+  constexpr int NC = GQ * NG;                 // (group, head) combos
+  constexpr int NT = (NC + 7) / 8;            // 8-combo tiles (QK M-tiles / PV N-tiles)
+  constexpr int RB = 16 * BITS;               // packed row bytes (d = 128)
+  constexpr int G = 128 / NG;
+  constexpr int CPB = 8 / BITS;
+  constexpr int VW = RB / 8;                  // V words per lane per 16-token tile (4 or 8)
+  constexpr uint32_t kCodeMask = BITS == 2 ? 0x00030003u : 0x000F000Fu;
+  constexpr uint32_t kByteMask = BITS == 2 ? 0x03030303u : 0x0F0F0F0Fu;
+  extern __shared__ __align__(128) unsigned char smem[];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gid = lane >> 2, t = lane & 3;
+  const int page_bytes = p.page_bytes, P = p.P;
+  unsigned char* ring = smem + (size_t)warp * S * page_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)kWarps * S * page_bytes) + warp * S;
+
+  if (lane == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  }
+  __syncwarp();
+  uint64_t policy;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(policy));
+
+  const int n_items = p.n_items;
+  auto fetch_async = [&]() { return lane == 0 ? atomicAdd(p.work, 1) : 0; };
+  auto bcast = [&](int v) { return __shfl_sync(0xffffffffu, v, 0); };
+  int cur = bcast(fetch_async());
+  int nxt = bcast(fetch_async());
+  int pending = fetch_async();                // the item after nxt (broadcast when needed)
+  Item Icur = decode_item(p, cur < n_items ? cur : 0);
+  Item Inxt = decode_item(p, nxt < n_items ? nxt : 0);
+  // load cursor: page lq_k of (lq_sel ? nxt : cur); global page sequence numbers
+  int lq_sel = 0, lq_k = 0;
+  uint32_t seq_issue = 0, seq_use = 0;
+  auto try_issue = [&]() {
+    while ((int)(seq_issue - seq_use) < S) {
+      const bool on_next = lq_sel != 0;
+      if ((on_next ? nxt : cur) >= n_items) break;
+      const Item& L = on_next ? Inxt : Icur;
+      if (lq_k >= L.np) {
+        if (!on_next) { lq_sel = 1; lq_k = 0; continue; }
+        break;
+      }
+      if (lane == 0) {
+        const int s = seq_issue % S;
+        const int64_t page = p.page_table[(size_t)L.b * p.max_pages + L.page0 + lq_k];
+        bulk_load(ring + (size_t)s * page_bytes, p.pool + (page * p.hkv + L.h) * (int64_t)page_bytes,
+                  page_bytes, &bars[s], policy);
+      }
+      ++seq_issue;
+      ++lq_k;
+    }
+  };
+
+  const int hh = gid % GQ;                    // every tile of this lane serves head hh
+  const bool real = NC >= 8 || gid < NC;
+
+  while (cur < n_items) {
+    const Item& I = Icur;
+    const size_t qrow = (size_t)I.b * p.hq + (size_t)I.h * GQ + hh;
+    const float qscale = real ? p.qscale[qrow] : 0.f;
+    int grp_of[NT];
+    float qsumf[NT];
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      const int c = 8 * j + gid;
+      grp_of[j] = c < NC ? c / GQ : 0;
+      qsumf[j] = c < NC ? (float)p.qsum[qrow * 8 + grp_of[j]] : 0.f;
+    }
+    uint32_t aq[NT][4][4];
+    {
+      const uint32_t* qf = p.qfrag + ((size_t)I.b * p.hkv + I.h) * NT * 16 * 32 + lane;
+#pragma unroll
+      for (int j = 0; j < NT; ++j)
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+          for (int r = 0; r < 4; ++r) aq[j][kk][r] = qf[(j * 16 + kk * 4 + r) * 32];
+    }
+    float acc[8][NT][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < NT; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.f;
+    float m_run = -INFINITY, l_run = 0.f;
+    float mv_acc[NT];
+#pragma unroll
+    for (int j = 0; j < NT; ++j) mv_acc[j] = 0.f;
+
+    // one page: chunks of up to 4 sub-tiles (64 tokens); FULL = no masking needed
+    auto page_body = [&](const unsigned char* pg, int valid, auto full_c) {
+      constexpr bool FULL = decltype(full_c)::value;
+      const unsigned char* vcodes = pg + p.vcodes_off;
+      const unsigned char* meta = pg + p.meta_off;
+      const int n_sub = FULL ? (P >> 4) : ((valid + 15) >> 4);
+      for (int c0 = 0; c0 < n_sub; c0 += 4) {
+        float sc[4][4];
+        float tmax = -INFINITY;
+#pragma unroll
+        for (int sl = 0; sl < 4; ++sl) {
+          const int st = c0 + sl;
+          if (st >= n_sub) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) sc[sl][e] = -INFINITY;
+            continue;
+          }
+          // ---- QK: B = K codes of tokens 2n + nt of the tile
+          int cq[NT][2][4];
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) {
+            uint32_t w[BITS];
+            const unsigned char* row = pg + (size_t)(16 * st + 8 * nt + gid) * RB + t * (RB / 4);
+            if (BITS == 2) {
+              const uint2 u = *reinterpret_cast<const uint2*>(row);
+              w[0] = u.x; w[1] = u.y;
+            } else {
+              const uint4 u = *reinterpret_cast<const uint4*>(row);
+              w[0] = u.x; w[1] = u.y; w[2 % BITS] = u.z; w[3 % BITS] = u.w;
+            }
+#pragma unroll
+            for (int j = 0; j < NT; ++j)
+#pragma unroll
+              for (int e = 0; e < 4; ++e) cq[j][nt][e] = 0;
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              uint32_t b0, b1;
+              if (BITS == 2) {
+                b0 = (w[0] >> (2 * kk)) & kByteMask;
+                b1 = (w[1] >> (2 * kk)) & kByteMask;
+              } else {
+                b0 = (w[kk >> 1] >> (4 * (kk & 1))) & kByteMask;
+                b1 = (w[2 + (kk >> 1)] >> (4 * (kk & 1))) & kByteMask;
+              }
+#pragma unroll
+              for (int j = 0; j < NT; ++j) imma16832(cq[j][nt], aq[j][kk], b0, b1);
+            }
+          }
+          // ---- scores of tokens 4t + e for head hh (log2 domain)
+          float part[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int j = 0; j < NT; ++j) {
+            const uint4 mk4 = *reinterpret_cast<const uint4*>(meta + 128 * NG * st + 128 * grp_of[j] + 32 * t);
+            const uint32_t mw[4] = {mk4.x, mk4.y, mk4.z, mk4.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int nt = e & 1, col = e >> 1;   // token 4t+e <-> (N-tile e&1, column 2t + e/2)
+              const int dot = cq[j][nt][col] * 256 + cq[j][nt][2 + col];
+              const __half2 smk = *reinterpret_cast<const __half2*>(&mw[e]);
+              part[e] = fmaf(__low2float(smk), (float)dot, fmaf(__high2float(smk), qsumf[j], part[e]));
+            }
+          }
+#pragma unroll
+          for (int x = GQ; x < 8 && x < NC; x <<= 1)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) part[e] += __shfl_xor_sync(0xffffffffu, part[e], x * 4);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            bool ok = real;
+            if (!FULL) ok = ok && (16 * st + 4 * t + e) < valid;
+            sc[sl][e] = ok ? part[e] * qscale : -INFINITY;
+            tmax = fmaxf(tmax, sc[sl][e]);
+          }
+        }
+        tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 1));
+        tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 2));
+        // ---- lazy online-softmax rescale (threshold 2^8)
+        const bool need = tmax > m_run + 8.f;
+        if (__any_sync(0xffffffffu, need)) {
+          const float m_new = need ? tmax : m_run;
+          const float alpha = need ? exp2f(m_run - m_new) : 1.f;
+          l_run *= alpha;
+#pragma unroll
+          for (int j = 0; j < NT; ++j) mv_acc[j] *= alpha;
+          m_run = m_new;
+          const float a0 = __shfl_sync(0xffffffffu, alpha, 8 * t);
+          const float a1 = __shfl_sync(0xffffffffu, alpha, 8 * t + 4);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < NT; ++j) {
+              acc[i][j][0] *= a0; acc[i][j][2] *= a0;
+              acc[i][j][1] *= a1; acc[i][j][3] *= a1;
+            }
+        }
+        // ---- PV per sub-tile
+#pragma unroll
+        for (int sl = 0; sl < 4; ++sl) {
+          const int st = c0 + sl;
+          if (st >= n_sub) break;
+          float pr[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            pr[e] = exp2f(sc[sl][e] - m_run);      // exp2(-inf) = 0 (m_run finite here)
+            l_run += pr[e];
+          }
+          uint32_t bpv[NT][2];
+#pragma unroll
+          for (int j = 0; j < NT; ++j) {
+            const uint4 mv4 = *reinterpret_cast<const uint4*>(meta + 128 * NG * st + 128 * grp_of[j] + 32 * t + 16);
+            const uint32_t mw[4] = {mv4.x, mv4.y, mv4.z, mv4.w};
+            float w4[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const __half2 smv = *reinterpret_cast<const __half2*>(&mw[e]);
+              if (FULL) {
+                w4[e] = pr[e] * __low2float(smv);
+                mv_acc[j] = fmaf(pr[e], __high2float(smv), mv_acc[j]);
+              } else {   // masked tokens may carry garbage metadata: keep them out
+                w4[e] = pr[e] == 0.f ? 0.f : pr[e] * __low2float(smv);
+                mv_acc[j] = pr[e] == 0.f ? mv_acc[j] : fmaf(pr[e], __high2float(smv), mv_acc[j]);
+              }
+            }
+            bpv[j][0] = pack_half2(w4[0], w4[2]);   // k-slots 2t, 2t+1 <-> tokens 4t, 4t+2
+            bpv[j][1] = pack_half2(w4[1], w4[3]);   // k-slots 2t+8, 2t+9 <-> tokens 4t+1, 4t+3
+          }
+          uint32_t vw[VW];
+          {
+            const uint4* vp = reinterpret_cast<const uint4*>(vcodes + (size_t)st * 16 * RB) + 4 * gid + t;
+#pragma unroll
+            for (int u = 0; u < VW / 4; ++u) {
+              const uint4 x = vp[32 * u];
+              vw[4 * u] = x.x; vw[4 * u + 1] = x.y; vw[4 * u + 2] = x.z; vw[4 * u + 3] = x.w;
+            }
+          }
+          uint32_t vs[VW];
+#pragma unroll
+          for (int k = 0; k < VW; ++k) vs[k] = vw[k] >> 8;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int q = i % CPB;
+            const uint32_t msk = kCodeMask << (BITS * q);
+            uint32_t a[4];
+            a[0] = vw[i / CPB] & msk;             // row gid,   tokens (4t, 4t+2)
+            a[1] = vw[VW / 2 + i / CPB] & msk;    // row gid+8, tokens (4t, 4t+2)
+            a[2] = vs[i / CPB] & msk;             // row gid,   tokens (4t+1, 4t+3)
+            a[3] = vs[VW / 2 + i / CPB] & msk;    // row gid+8, tokens (4t+1, 4t+3)
+#pragma unroll
+            for (int j = 0; j < NT; ++j) hmma16816(acc[i][j], a, bpv[j][0], bpv[j][1]);
+          }
+        }
+      }
+    };
+
+    try_issue();
+    for (int k = 0; k < I.np; ++k) {
+      const int s = seq_use % S;
+      mbar_wait(&bars[s], (seq_use / S) & 1);
+      const unsigned char* pg = ring + (size_t)s * page_bytes;
+      const int valid = min(P, I.seq_len - (I.page0 + k) * P);
+      if (valid == P) page_body(pg, valid, std::true_type{});
+      else page_body(pg, valid, std::false_type{});
+      // release the stage, keep the ring full (possibly with the next item's pages)
+      __syncwarp();
+      ++seq_use;
+      if (lane == 0) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      try_issue();
+    }
+
+    // ---- write this item's partial (unnormalized õ in the rotated frame, m, l)
+    l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
+    l_run += __shfl_xor_sync(0xffffffffu, l_run, 2);
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      mv_acc[j] += __shfl_xor_sync(0xffffffffu, mv_acc[j], 1);
+      mv_acc[j] += __shfl_xor_sync(0xffffffffu, mv_acc[j], 2);
+    }
+    const size_t row0 = ((size_t)I.b * p.hq + (size_t)I.h * GQ) * p.n_splits + I.split;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float unscale = (float)(1 << (24 - BITS * (i % CPB)));
+#pragma unroll
+      for (int j = 0; j < NT; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int col = 2 * t + (e & 1);
+          const int cc = 8 * j + col;
+          const int ch = pv_channel<BITS>(i, gid, e >> 1);
+          const float mvs = __shfl_sync(0xffffffffu, mv_acc[j], 4 * col);
+          if (cc < NC && ch / G == cc / GQ) {
+            const size_t row = row0 + (size_t)(cc % GQ) * p.n_splits;
+            p.ws_o[row * 128 + ch] = fmaf(acc[i][j][e], unscale, mvs);
+          }
+        }
+    }
+    if (t == 0 && gid < GQ) {
+      const size_t row = row0 + (size_t)gid * p.n_splits;
+      p.ws_m[row] = m_run;
+      p.ws_l[row] = l_run;
+    }
+    // ---- advance: the loader already moved on to `nxt`
+    cur = nxt;
+    Icur = Inxt;
+    if (lq_sel) lq_sel = 0; else lq_k = 0;
+    nxt = cur < n_items ? bcast(pending) : n_items;
+    if (nxt < n_items) Inxt = decode_item(p, nxt);
+    pending = nxt < n_items ? fetch_async() : 0;
+  }
+}
+
+// ---------------------------------------------------------------- dispatch
+namespace {
+using KernelFn = void (*)(AttnParams, int);
+
+template <int BITS>
+KernelFn pick_g(int g, int ng) {
+#define OSCAR_CASE(GQ_, NG_) \
+  if (g == GQ_ && ng == NG_) return attend_partial_mma<BITS, GQ_, NG_>;
+  OSCAR_CASE(1, 1) OSCAR_CASE(1, 2) OSCAR_CASE(1, 4)
+  OSCAR_CASE(2, 1) OSCAR_CASE(2, 2) OSCAR_CASE(2, 4)
+  OSCAR_CASE(4, 1) OSCAR_CASE(4, 2) OSCAR_CASE(4, 4)
+  OSCAR_CASE(8, 1) OSCAR_CASE(8, 2)
+#undef OSCAR_CASE
+  return nullptr;
+}
+
+KernelFn pick(int bits, int g, int ng) {
+  if (bits == 2) return pick_g<2>(g, ng);
+  if (bits == 4) return pick_g<4>(g, ng);
+  return nullptr;
+}
+
+int stages_for(int page_bytes) {
+  const int S = (48 * 1024) / (kWarps * page_bytes);
+  return S < 2 ? 2 : (S > 4 ? 4 : S);
+}
+}  // namespace
+
+bool attend_mma_supported(const oscar_ctx& c) {
+  return c.d == 128 && pick(c.bits, c.g, c.ng) != nullptr && c.P % 16 == 0;
+}
+
+int attend_mma_total_warps(const oscar_ctx& c) {
+  KernelFn fn = pick(c.bits, c.g, c.ng);
+  if (!fn) return 0;
+  const int S = stages_for(c.page_bytes);
+  const int smem = kWarps * S * (c.page_bytes + 8);
+  int per_sm = 0;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kWarps * 32, smem) != cudaSuccess) {
+    cudaGetLastError();
+    per_sm = 2;
+  }
+  return c.num_sms * (per_sm > 0 ? per_sm : 1) * kWarps;
+}
+
+cudaError_t launch_attend_mma(const AttnParams& p, int total_warps, cudaStream_t s) {
+  KernelFn fn = pick(p.bits, p.g, p.ng);
+  if (!fn) return cudaErrorNotSupported;
+  const int S = stages_for(p.page_bytes);
+  const int smem = kWarps * S * (p.page_bytes + 8);
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  int warps = total_warps < p.n_items ? total_warps : p.n_items;
+  const int grid = (warps + kWarps - 1) / kWarps;
+  fn<<<grid, kWarps * 32, smem, s>>>(p, S);
+  return cudaGetLastError();
 }
 
 }  // namespace oscar

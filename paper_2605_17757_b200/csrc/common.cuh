@@ -46,18 +46,24 @@ __device__ __forceinline__ float bf16_to_f32(uint16_t b) {
 // ---------------------------------------------------------------- packed page FORMAT
 // (include/oscar.h).  Placement of rows / bytes inside one (page, head) block:
 //   K row u        -> row position fmt_krow(u) (even tokens of each 16-token tile first)
-//   V byte j of u  -> vcodes_off + fmt_vbyte(u, j, rb) (4-token groups, byte-interleaved,
-//                     word j stored at position (rb/8)(j%8) + j/8)
-//   meta (u, grp)  -> meta_off + fmt_meta(u, grp, ng): 8 B {s_K, m_K, s_V, m_V} fp16
+//   V byte j of u  -> vcodes_off + fmt_vbyte(u, j, rb): a 32-bit word holds byte j of the 4
+//                     tokens of a 4-token group; words are grouped in 16-byte chunks
+//                     (chunk 32·(k/4) + 4·(j%8) + group-in-tile, k = j/8) so that the
+//                     decode kernel's per-lane 16-byte loads are bank-conflict free
+//   meta (u, grp)  -> meta_off + fmt_meta(u, grp, ng): fp16 (s_K, m_K) at +0 and (s_V, m_V)
+//                     at +16 of a 32-B chunk [tile of 16][grp][group-in-tile]; the token in
+//                     its 4-token group selects the 4-byte slot
 __host__ __device__ __forceinline__ int fmt_krow(int u) {
   return 16 * (u >> 4) + 8 * (u & 1) + ((u & 15) >> 1);
 }
-__host__ __device__ __forceinline__ int fmt_vpos(int j, int rb) { return (rb >> 3) * (j & 7) + (j >> 3); }
 __host__ __device__ __forceinline__ int fmt_vbyte(int u, int j, int rb) {
-  return (u >> 2) * 4 * rb + 4 * fmt_vpos(j, rb) + (u & 3);
+  const int k = j >> 3, lane = 4 * (j & 7) + ((u >> 2) & 3);
+  const int word = ((rb >> 3) & 3) == 0 ? 128 * (k >> 2) + 4 * lane + (k & 3) : 32 * k + lane;
+  return 16 * rb * (u >> 4) + 4 * word + (u & 3);
 }
+// offset of the (s_K, m_K) pair; the (s_V, m_V) pair is at +16
 __host__ __device__ __forceinline__ int fmt_meta(int u, int grp, int ng) {
-  return (u >> 2) * 32 * ng + 32 * grp + 8 * (u & 3);
+  return 128 * ng * (u >> 4) + 128 * grp + 32 * ((u >> 2) & 3) + 4 * (u & 3);
 }
 
 }  // namespace oscar

@@ -93,12 +93,14 @@ def _decode_pool(pool, slots, H, fmt):
     return out
 
 
-@pytest.mark.parametrize("bits,G,rho,variant", [(2, 64, (1.0, 1.0), 0), (4, 32, (0.96, 0.92), 0),
-                                                (2, 64, (1.0, 1.0), 1)])
-def test_quantize_append_parity(bits, G, rho, variant):
+@pytest.mark.parametrize("bits,G,rho,variant,Tn", [(2, 64, (1.0, 1.0), 0, 1000), (4, 32, (0.96, 0.92), 0, 1000),
+                                                   (2, 64, (1.0, 1.0), 1, 1000), (2, 32, (1.0, 1.0), 0, 16),
+                                                   (4, 64, (1.0, 1.0), 0, 300), (4, 32, (1.0, 1.0), 0, 1280),
+                                                   (2, 128, (1.0, 1.0), 0, 129)])
+def test_quantize_append_parity(bits, G, rho, variant, Tn):
     torch = _torch()
-    rng = np.random.default_rng(7 + bits + G)
-    H, Tn, npages = 8, 1000, 20
+    rng = np.random.default_rng(7 + bits + G + Tn)
+    H, npages = 8, 21
     fmt = O.PageFormat(128, bits, G, 64)
     K = synth.gen_keys(rng, Tn, H, 128)
     V = synth.gen_values(rng, Tn, H, 128)

@@ -417,11 +417,18 @@ def test_page_format_and_paged_roundtrip():
         rb = fmt.row_bytes
         c, _, _ = O.quantize_rows(Vr[:1, 0], bits, G)
         packed = O.pack_codes(c, bits)[0]
-        grp_base = fmt.vcodes_off + (off // 4) * 4 * rb + off % 4
-        inv = np.zeros(rb, np.int64)
-        for j in range(rb):
-            inv[(rb // 8) * (j % 8) + j // 8] = j
-        assert np.array_equal(pool[page, 0, grp_base: grp_base + 4 * rb: 4], packed[inv])
+        # word k of chunk (gid = j % 8): byte j of the 4 tokens of the row's group
+        for j in ([0, 1, 7, 8, rb - 1] if bits != 3 else []):
+            k = j // 8
+            o = (fmt.vcodes_off + 16 * rb * (off // 16) + 16 * (32 * (k // 4) + 4 * (j % 8) + (off // 4) % 4)
+                 + 4 * (k % 4) + off % 4)
+            assert pool[page, 0, o] == packed[j]
+        offs = np.concatenate([fmt.vbyte_offsets(u) for u in range(64)])
+        assert len(set(offs.tolist())) == 64 * rb and offs.min() == fmt.vcodes_off \
+            and offs.max() == fmt.vcodes_off + 64 * rb - 1                # a bijection on the region
+        mo = [o for u in range(64) for g_ in range(128 // G) for o in fmt.meta_offsets(u, g_)]
+        assert len(set(mo)) == len(mo) and min(mo) == fmt.meta_off
+        assert max(mo) + 4 == fmt.meta_off + 64 * (128 // G) * 8 <= fmt.page_bytes
         c, _, _ = O.quantize_rows(Kr[:1, 0], bits, G)
         kpos = 16 * (off // 16) + 8 * (off % 2) + (off % 16) // 2
         assert np.array_equal(pool[page, 0, kpos * rb: (kpos + 1) * rb], O.pack_codes(c, bits)[0])

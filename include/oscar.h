@@ -133,6 +133,21 @@ OSCAR_API oscar_status oscar_attend(const oscar_ctx* ctx, const void* q, const i
                           void* workspace, size_t workspace_bytes, void* out, int32_t out_fp32,
                           float* lse, void* stream);
 
+/* attend over the mixed-precision cache (§4 "KV Cache Layout" P:L537-548: bf16 sink ‖ INT2
+ * history ‖ bf16 recent window; Alg. 1 DecodeStep P:L1627-1635): the INT2 history is the first
+ * seq_lens[b] tokens of page_table[b] in the pool (as oscar_attend), and the bf16 tokens (sink +
+ * recent, RAW rows as appended, Alg. 1) are seg_k / seg_v: bf16
+ * [B][H_kv][seg_cap][d], the first seg_lens[b] rows valid (their order is irrelevant).  A third
+ * kernel computes the bf16 partial (original frame) and the same LSE merge combines it with the
+ * INT2 partials.  1 <= seg_cap <= 1024.  Demotion of the oldest recent row is the
+ * caller's oscar_quantize_append of that row.  Other arguments as oscar_attend. */
+OSCAR_API oscar_status oscar_attend_mixed(const oscar_ctx* ctx, const void* q, const int32_t* page_table,
+                                const int32_t* seq_lens, int32_t B, int32_t max_pages, const void* pool,
+                                const float* R_K, const float* R_V, const void* seg_k, const void* seg_v,
+                                const int32_t* seg_lens, int32_t seg_cap, void* workspace,
+                                size_t workspace_bytes, void* out, int32_t out_fp32, float* lse,
+                                void* stream);
+
 /* ---------------------------------------------------------------- test hooks
  * Stage-isolated entry points used by the parity tests (same kernels, other I/O).
  * oscar_rotate: Xrot[t][h][:] = X[t][h][:] · R[h] in fp32 (App A.5).

@@ -19,7 +19,7 @@ __all__ = [
     "cov_accumulate", "score_value", "calibrate_from_sums", "rotate", "clip_index",
     "clip_rows", "quantize_rows", "dequantize_rows", "pack_codes", "unpack_codes",
     "PageFormat", "quantize_rotated", "quantize_append", "read_rows", "attend_rows",
-    "attend", "attend_alg1", "residual_cov", "group_ranges", "effective_bpe",
+    "attend", "attend_mixed", "attend_alg1", "residual_cov", "group_ranges", "effective_bpe",
 ]
 
 
@@ -417,6 +417,41 @@ def attend(q, page_table, seq_lens, pool, R_K, R_V, fmt: PageFormat, num_kv_head
             ob, lb = attend_rows(q[b, h * g:(h + 1) * g], Kh, Vh, R_K[h], R_V[h], scale)
             o[b, h * g:(h + 1) * g] = ob
             lse[b, h * g:(h + 1) * g] = lb
+    return o, lse
+
+
+def attend_mixed(q, page_table, seq_lens, pool, seg_k, seg_v, seg_lens, R_K, R_V, fmt: PageFormat,
+                 num_kv_heads: int, scale=None):
+    """Mixed-precision decode attention (§4; Alg. 1 DecodeStep P:L1632-1635,
+    NEXT-1): the logical cache is the bf16 tokens of the segment (sink + recent, raw rows,
+    seg_k/seg_v [B][H_kv][cap][d], first seg_lens[b] valid) plus the INT2 history in the paged
+    pool (first seq_lens[b] tokens of the page table).  Written in the original frame exactly as
+    Alg. 1: K̂_hist = Q(K̃)R_Kᵀ, V̂_hist = Q(Ṽ)R_Vᵀ, K_all = Concat(sink, K̂_hist, recent),
+    o = softmax(scale · q K_allᵀ) V_all (token order does not change the result).
+    Returns (o [B, H_q, d] fp64, lse [B, H_q])."""
+    q = np.asarray(q, dtype=np.float64)
+    B, Hq, d = q.shape
+    g = Hq // num_kv_heads
+    if scale is None:
+        scale = 1.0 / math.sqrt(d)
+    o = np.zeros((B, Hq, d))
+    lse = np.full((B, Hq), -np.inf)
+    for b in range(B):
+        slots = _slots_of(page_table[b], int(seq_lens[b]), fmt.P)
+        for h in range(num_kv_heads):
+            Kh, Vh = read_rows(pool, slots, h, fmt)
+            K_all = np.concatenate([Kh @ np.asarray(R_K[h], np.float64).T,
+                                    np.asarray(seg_k[b, h, :seg_lens[b]], np.float64)])
+            V_all = np.concatenate([Vh @ np.asarray(R_V[h], np.float64).T,
+                                    np.asarray(seg_v[b, h, :seg_lens[b]], np.float64)])
+            if K_all.shape[0] == 0:
+                continue
+            logits = scale * (q[b, h * g:(h + 1) * g] @ K_all.T)
+            mx = logits.max(axis=1, keepdims=True)
+            e = np.exp(logits - mx)
+            l = e.sum(axis=1, keepdims=True)
+            o[b, h * g:(h + 1) * g] = (e / l) @ V_all
+            lse[b, h * g:(h + 1) * g] = (mx + np.log(l))[:, 0]
     return o, lse
 
 

@@ -22,8 +22,8 @@ OK, ERR_ARG, ERR_DIM, ERR_UNSUPPORTED, ERR_CUDA, ERR_CONVERGENCE = range(6)
 EXPORTED = [
     "oscar_create", "oscar_destroy", "oscar_last_error", "oscar_version", "oscar_page_bytes",
     "oscar_calib_accumulate", "oscar_calib_finalize", "oscar_quantize_append",
-    "oscar_attend_workspace_bytes", "oscar_attend", "oscar_rotate", "oscar_quantize_rotated",
-    "oscar_set_variant",
+    "oscar_attend_workspace_bytes", "oscar_attend", "oscar_attend_mixed", "oscar_rotate",
+    "oscar_quantize_rotated", "oscar_set_variant",
 ]
 
 
@@ -50,6 +50,8 @@ _sig = {
     "oscar_attend_workspace_bytes": (_sz, [_vp, _i32, _i32]),
     "oscar_attend": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _vp, _i32,
                             _vp, _vp]),
+    "oscar_attend_mixed": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i32,
+                                  _vp, _sz, _vp, _i32, _vp, _vp]),
     "oscar_rotate": (_i32, [_vp, _vp, _vp, _vp, _i64, _vp]),
     "oscar_quantize_rotated": (_i32, [_vp, _vp, _vp, _vp, _i64, _vp, _vp]),
     "oscar_set_variant": (_i32, [_vp, _i32]),
@@ -114,9 +116,9 @@ class Oscar:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and _lib is not None and getattr(_lib, "oscar_destroy", None) is not None:
             _lib.oscar_destroy(h)
-            self._h = None
+        self._h = None
 
     # ---------------------------------------------------------------- layout
     def page_bytes(self) -> int:
@@ -153,6 +155,16 @@ class Oscar:
                                  page_table.shape[1], _ptr(pool), _ptr(R_K), _ptr(R_V),
                                  _ptr(workspace), workspace.numel() * workspace.element_size(),
                                  _ptr(out), out_fp32, _ptr(lse), _stream(stream)), "oscar_attend")
+
+    def attend_mixed(self, q, page_table, seq_lens, pool, R_K, R_V, seg_k, seg_v, seg_lens, workspace,
+                     out, lse=None, stream=None):
+        import torch
+        out_fp32 = 1 if out.dtype == torch.float32 else 0
+        _check(_lib.oscar_attend_mixed(self._h, _ptr(q), _ptr(page_table), _ptr(seq_lens), q.shape[0],
+                                       page_table.shape[1], _ptr(pool), _ptr(R_K), _ptr(R_V), _ptr(seg_k),
+                                       _ptr(seg_v), _ptr(seg_lens), seg_k.shape[2], _ptr(workspace),
+                                       workspace.numel() * workspace.element_size(), _ptr(out), out_fp32,
+                                       _ptr(lse), _stream(stream)), "oscar_attend_mixed")
 
     # ---------------------------------------------------------------- test hooks
     def rotate(self, X, R, Xrot, stream=None):

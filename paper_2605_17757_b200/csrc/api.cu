@@ -17,6 +17,12 @@ cudaError_t launch_append_tc(const oscar_ctx& c, const void* K, const void* V,
                              const int64_t* slots, int64_t T, const float* RK, const float* RV,
                              void* pool, cudaStream_t s);
 bool append_tc_supported(const oscar_ctx& c);
+bool cov_tc_supported(const oscar_ctx& c);
+bool append_small_ok(const oscar_ctx& c, int64_t T);
+cudaError_t launch_append_small(const oscar_ctx& c, const void* K, const void* V, const int64_t* slots,
+                                int64_t T, const float* RK, const float* RV, void* pool, cudaStream_t s);
+cudaError_t launch_cov_accum_tc(const oscar_ctx& c, const void* Q, const void* SV, int64_t N, double* acc,
+                                cudaStream_t s);
 }  // namespace oscar
 
 namespace {
@@ -116,6 +122,8 @@ oscar_status oscar_calib_accumulate(const oscar_ctx* ctx, const void* Q, const v
   if (N < 0) return fail(OSCAR_ERR_ARG, "N must be >= 0 (got %lld)", (long long)N);
   if (N == 0) return OSCAR_OK;
   if (!Q || !SV || !acc) return fail(OSCAR_ERR_ARG, "oscar_calib_accumulate: NULL pointer");
+  if (ctx->variant == 0 && oscar::cov_tc_supported(*ctx))
+    return cuda_status(oscar::launch_cov_accum_tc(*ctx, Q, SV, N, acc, as_stream(stream)), "cov_accum_tc");
   return cuda_status(oscar::launch_cov_accum(*ctx, Q, SV, N, acc, as_stream(stream)), "cov_accum");
 }
 
@@ -152,6 +160,8 @@ oscar_status oscar_quantize_append(const oscar_ctx* ctx, const void* K, const vo
   if (T == 0) return OSCAR_OK;
   if (!K || !V || !slots || !R_K || !R_V || !pool) return fail(OSCAR_ERR_ARG, "oscar_quantize_append: NULL pointer");
   cudaStream_t s = as_stream(stream);
+  if (ctx->variant == 0 && oscar::append_small_ok(*ctx, T))      // decode-size: latency path
+    return cuda_status(oscar::launch_append_small(*ctx, K, V, slots, T, R_K, R_V, pool, s), "append_small");
   if (ctx->variant == 0 && oscar::append_tc_supported(*ctx))
     return cuda_status(oscar::launch_append_tc(*ctx, K, V, slots, T, R_K, R_V, pool, s), "append_tc");
   return cuda_status(oscar::launch_append_simple(*ctx, 0, K, V, nullptr, nullptr, slots, T, R_K, R_V,
@@ -200,8 +210,33 @@ oscar_status oscar_attend(const oscar_ctx* ctx, const void* q, const int32_t* pa
   if (workspace_bytes < need)
     return fail(OSCAR_ERR_ARG, "workspace too small: %zu < %zu", workspace_bytes, need);
   return cuda_status(oscar::launch_attend(*ctx, q, page_table, seq_lens, B, max_pages, pool, R_K, R_V,
-                                          workspace, out, out_fp32, lse, as_stream(stream)),
+                                          workspace, out, out_fp32, lse, as_stream(stream), nullptr,
+                                          nullptr, nullptr, 0),
                      "attend");
+}
+
+oscar_status oscar_attend_mixed(const oscar_ctx* ctx, const void* q, const int32_t* page_table,
+                                const int32_t* seq_lens, int32_t B, int32_t max_pages, const void* pool,
+                                const float* R_K, const float* R_V, const void* seg_k, const void* seg_v,
+                                const int32_t* seg_lens, int32_t seg_cap, void* workspace,
+                                size_t workspace_bytes, void* out, int32_t out_fp32, float* lse,
+                                void* stream) {
+  if (!ctx) return fail(OSCAR_ERR_ARG, "NULL ctx");
+  if (B < 0 || max_pages < 0 || seg_cap < 0) return fail(OSCAR_ERR_ARG, "negative size");
+  if (B == 0) return OSCAR_OK;
+  if (max_pages == 0) return fail(OSCAR_ERR_ARG, "max_pages must be > 0");
+  if (seg_cap == 0 || seg_cap > 1024)
+    return fail(OSCAR_ERR_ARG, "seg_cap must be in [1, 1024] (got %d)", seg_cap);
+  if (!q || !page_table || !seq_lens || !pool || !R_K || !R_V || !workspace || !out || !seg_k || !seg_v ||
+      !seg_lens)
+    return fail(OSCAR_ERR_ARG, "oscar_attend_mixed: NULL pointer");
+  const size_t need = oscar::attend_workspace_bytes(*ctx, B, max_pages);
+  if (workspace_bytes < need)
+    return fail(OSCAR_ERR_ARG, "workspace too small: %zu < %zu", workspace_bytes, need);
+  return cuda_status(oscar::launch_attend(*ctx, q, page_table, seq_lens, B, max_pages, pool, R_K, R_V,
+                                          workspace, out, out_fp32, lse, as_stream(stream), seg_k, seg_v,
+                                          seg_lens, seg_cap),
+                     "attend_mixed");
 }
 
 }  // extern "C"

@@ -23,6 +23,7 @@ __global__ void __launch_bounds__(128) append_simple_kernel(
   float* xs = sm + kD * kD;             // [kAppTok][128]
   float* ys = xs + kAppTok * kD;        // [kAppTok][128]
   const int h = blockIdx.y, isV = blockIdx.z;
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");   // PDL (see append_tc.cu)
   const int64_t t0 = (int64_t)blockIdx.x * kAppTok;
   const int nt = (int)((T - t0) < (int64_t)kAppTok ? (T - t0) : (int64_t)kAppTok);
   const int tid = threadIdx.x;
@@ -81,6 +82,49 @@ cudaError_t launch_append_simple(const oscar_ctx& c, int mode, const void* K, co
   append_simple_kernel<<<grid, 128, smem, s>>>(
       mode, static_cast<const uint16_t*>(K), static_cast<const uint16_t*>(V), Krot, Vrot, slots,
       T, RK, RV, static_cast<uint8_t*>(pool), rot_out, make_epi_params(c));
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------
+// Decode-size appends (a few tokens): latency-bound, so one CTA per (token, head, K|V) row.
+// Thread c forms x̃_c = Σ_k x_k R[k][c] in fp32 with R read straight from L2 (coalesced
+// columns, 32 loads in flight), then warp 0 runs the shared quantize/pack/store epilogue.
+// ------------------------------------------------------------------------------------
+constexpr int kSmallAppendMaxT = 64;
+
+__global__ void __launch_bounds__(128) append_small_kernel(const uint16_t* __restrict__ K,
+                                                           const uint16_t* __restrict__ V,
+                                                           const int64_t* __restrict__ slots,
+                                                           const float* __restrict__ RK,
+                                                           const float* __restrict__ RV,
+                                                           uint8_t* __restrict__ pool, EpiParams ep) {
+  __shared__ __align__(16) float xs[kD];
+  __shared__ __align__(16) float ys[kD];
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");   // PDL (see append_tc.cu)
+  const int t = blockIdx.x, h = blockIdx.y, isV = blockIdx.z, c = threadIdx.x;
+  const uint16_t* X = isV ? V : K;
+  xs[c] = bf16_to_f32(X[((int64_t)t * ep.hkv + h) * kD + c]);
+  __syncthreads();
+  const float* R = (isV ? RV : RK) + (size_t)h * kD * kD + c;
+  float acc = 0.f;
+#pragma unroll 32
+  for (int k = 0; k < kD; ++k) acc = fmaf(xs[k], R[(size_t)k * kD], acc);
+  ys[c] = acc;
+  __syncthreads();
+  if (c < 32) {
+    const float4 y4 = reinterpret_cast<const float4*>(ys)[c];
+    float y[4] = {y4.x, y4.y, y4.z, y4.w};
+    quantize_store_row_warp(ep, y, c, slots[t], h, isV, pool);
+  }
+}
+
+bool append_small_ok(const oscar_ctx& c, int64_t T) { return T <= kSmallAppendMaxT && c.bits != 3; }
+
+cudaError_t launch_append_small(const oscar_ctx& c, const void* K, const void* V, const int64_t* slots,
+                                int64_t T, const float* RK, const float* RV, void* pool, cudaStream_t s) {
+  append_small_kernel<<<dim3((unsigned)T, c.hkv, 2), 128, 0, s>>>(
+      static_cast<const uint16_t*>(K), static_cast<const uint16_t*>(V), slots, RK, RV,
+      static_cast<uint8_t*>(pool), make_epi_params(c));
   return cudaGetLastError();
 }
 

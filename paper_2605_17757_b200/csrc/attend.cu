@@ -12,93 +12,90 @@
 namespace oscar {
 
 // ------------------------------------------------------------------ q rotation
-// grid (B, H_kv); 128 threads: thread c computes column c of q̃ for the g heads of the group.
-// Also emits the 15-bit integer form used by the IMMA QK path: qscale = max|q̃| / 32639,
+// grid (B, H_kv); one warp per query head of the group (g warps).  Lane l computes columns
+// 4l..4l+3 of q̃ = q · R_K[h] · scale · log2(e) (fp32, kept for the simple kernel), then the
+// 15-bit integer form used by the IMMA QK path: qscale = max|q̃| / 32639,
 // qint = rint(q̃ / qscale) (|qint| <= 32639 = 127·256 + 127, so hi/lo int8 never overflow),
-// qsum[grp] = Σ_{c in grp} qint.
-__global__ void __launch_bounds__(128) q_rotate_kernel(const uint16_t* __restrict__ q,
+// qsum[grp] = Σ_{c in grp} qint, and the per-lane IMMA A fragments of the group.
+// PDL: the work depends only on the caller's q and R_K; griddepcontrol.wait at the end keeps
+// "this kernel complete => the preceding kernel complete" for the partial kernel.
+__global__ void __launch_bounds__(256) q_rotate_kernel(const uint16_t* __restrict__ q,
                                                        const float* __restrict__ RK, int Hq,
-                                                       int g, int G, float qscale,
+                                                       int g, int lgG, float qscale,
                                                        float* __restrict__ qt,
                                                        int16_t* __restrict__ qint,
                                                        float* __restrict__ qsc,
                                                        int32_t* __restrict__ qsum,
                                                        uint32_t* __restrict__ qfrag, int bits,
                                                        int nt, int32_t* __restrict__ work) {
-  extern __shared__ __align__(16) float Rs[];            // R_K[h] staged: [128][128] fp32
-  __shared__ float qs[8][kD];
-  __shared__ float red[8][4];
-  __shared__ int gsum[8][8];
+  __shared__ __align__(16) float qs[8][kD];
   __shared__ int16_t qis[8][kD];
-  const int b = blockIdx.x, h = blockIdx.y, c = threadIdx.x;
-  const int warp = c >> 5, lane = c & 31;
-  if (work && b == 0 && h == 0 && c == 0) *work = 0;     // reset the work-item counter
+  const int b = blockIdx.x, h = blockIdx.y, tid = threadIdx.x;
+  const int w = tid >> 5, lane = tid & 31;
+  const int G = 1 << lgG;
+  const size_t row = (size_t)b * Hq + (size_t)h * g + w;
+  if (work && b == 0 && h == 0 && tid == 0) *work = 0;   // reset the work-item counter
   {
-    const float4* R4 = reinterpret_cast<const float4*>(RK + (size_t)h * kD * kD);
-#pragma unroll 8
-    for (int e = c; e < kD * kD / 4; e += 128) reinterpret_cast<float4*>(Rs)[e] = R4[e];
+    const uint2 u = reinterpret_cast<const uint2*>(q + row * kD)[lane];
+    float4 f;
+    f.x = __uint_as_float(u.x << 16); f.y = __uint_as_float(u.x & 0xffff0000u);
+    f.z = __uint_as_float(u.y << 16); f.w = __uint_as_float(u.y & 0xffff0000u);
+    reinterpret_cast<float4*>(qs[w])[lane] = f;
   }
-  for (int i = 0; i < g; ++i) qs[i][c] = bf16_to_f32(q[((size_t)b * Hq + h * g + i) * kD + c]);
-  if (c < 64) gsum[c >> 3][c & 7] = 0;
-  __syncthreads();
-  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-#pragma unroll 4
+  __syncwarp();
+  const float4* R4 = reinterpret_cast<const float4*>(RK + (size_t)h * kD * kD) + lane;
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll 16
   for (int k = 0; k < kD; ++k) {
-    const float r = Rs[k * kD + c];
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-      if (i < g) acc[i] = fmaf(qs[i][k], r, acc[i]);
+    const float4 r = R4[(size_t)k * (kD / 4)];
+    const float x = qs[w][k];
+    a0 = fmaf(x, r.x, a0); a1 = fmaf(x, r.y, a1); a2 = fmaf(x, r.z, a2); a3 = fmaf(x, r.w, a3);
   }
-  for (int i = 0; i < g; ++i) {
-    acc[i] *= qscale;
-    qt[((size_t)b * Hq + h * g + i) * kD + c] = acc[i];
-    float m = fabsf(acc[i]);
-    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (lane == 0) red[i][warp] = m;
-  }
+  a0 *= qscale; a1 *= qscale; a2 *= qscale; a3 *= qscale;
+  reinterpret_cast<float4*>(qt + row * kD)[lane] = make_float4(a0, a1, a2, a3);
+  float mx = fmaxf(fmaxf(fabsf(a0), fabsf(a1)), fmaxf(fabsf(a2), fabsf(a3)));
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  const float s = mx > 0.f ? mx / 32639.f : 1.f;
+  const int v0 = max(-32639, min(32639, __float2int_rn(a0 / s)));
+  const int v1 = max(-32639, min(32639, __float2int_rn(a1 / s)));
+  const int v2 = max(-32639, min(32639, __float2int_rn(a2 / s)));
+  const int v3 = max(-32639, min(32639, __float2int_rn(a3 / s)));
+  reinterpret_cast<uint2*>(qint + row * kD)[lane] =
+      make_uint2((uint32_t)(v0 & 0xffff) | ((uint32_t)v1 << 16), (uint32_t)(v2 & 0xffff) | ((uint32_t)v3 << 16));
+  reinterpret_cast<uint2*>(qis[w])[lane] =
+      make_uint2((uint32_t)(v0 & 0xffff) | ((uint32_t)v1 << 16), (uint32_t)(v2 & 0xffff) | ((uint32_t)v3 << 16));
+  if (lane == 0) qsc[row] = s;
+  int gs = v0 + v1 + v2 + v3;                      // lanes of one group: G/4 consecutive lanes
+  for (int o = 1; o < (G >> 2); o <<= 1) gs += __shfl_xor_sync(0xffffffffu, gs, o);
+  if ((lane & ((G >> 2) - 1)) == 0) qsum[row * 8 + (lane * 4 >> lgG)] = gs;
   __syncthreads();
-  for (int i = 0; i < g; ++i) {
-    const float mx = fmaxf(fmaxf(red[i][0], red[i][1]), fmaxf(red[i][2], red[i][3]));
-    const float s = mx > 0.f ? mx / 32639.f : 1.f;
-    const int v = max(-32639, min(32639, __float2int_rn(acc[i] / s)));
-    const size_t row = (size_t)b * Hq + h * g + i;
-    qint[row * kD + c] = (int16_t)v;
-    qis[i][c] = (int16_t)v;
-    if (c == 0) qsc[row] = s;
-    int ws = v;
-    for (int o = 16; o > 0; o >>= 1) ws += __shfl_xor_sync(0xffffffffu, ws, o);
-    if (lane == 0) atomicAdd(&gsum[i][(c / G)], ws);   // G >= 32: a warp lies in one group
-  }
-  __syncthreads();
-  if (c < g * 8) {
-    const int i = c >> 3, grp = c & 7;
-    qsum[((size_t)b * Hq + h * g + i) * 8 + grp] = gsum[i][grp];
-  }
   // IMMA A fragments for attend_partial_mma: word (j, kk, r) of lane (gid, t) holds the
   // hi (r even) / lo (r odd) int8 of qint[head][channel] for combo 8j + gid = grp·g + head,
   // zero outside the combo's group (see attend_mma.cu)
   if (qfrag) {
-    const int ng = kD / G, nc = g * ng;
+    const int nc = g << (7 - lgG);
     uint32_t* dst = qfrag + ((size_t)b * gridDim.y + h) * nt * 16 * 32;
-    for (int w = c; w < nt * 16 * 32; w += 128) {
-      const int ln = w & 31, rest = w >> 5;
+    for (int wd = tid; wd < nt * 16 * 32; wd += blockDim.x) {
+      const int ln = wd & 31, rest = wd >> 5;
       const int r = rest & 3, kk = (rest >> 2) & 3, j = rest >> 4;
       const int gid = ln >> 2, t = ln & 3, cb = 8 * j + gid;
       uint32_t v = 0;
       if (cb < nc) {
-        const int grp = cb / g, hd = cb % g;
+        const int grp = cb / g, hd = cb - grp * g;
+#pragma unroll
         for (int m = 0; m < 4; ++m) {
           const int ch = qk_channel(bits, kk, 4 * t + m + ((r & 2) ? 16 : 0));
-          if (ch / G != grp) continue;
+          if ((ch >> lgG) != grp) continue;
           const int qv = qis[hd][ch];
           const int hi8 = (qv + 128) >> 8;
           const int val = (r & 1) ? (qv - 256 * hi8) : hi8;
           v |= (uint32_t)(val & 0xff) << (8 * m);
         }
       }
-      dst[w] = v;
+      dst[wd] = v;
     }
   }
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
 }
 
 // ------------------------------------------------------------------ simple partial kernel
@@ -213,64 +210,156 @@ __global__ void __launch_bounds__(128) attend_partial_simple(AttnParams p) {
 }
 
 // ------------------------------------------------------------------ merge
-// grid (B·H_q); 128 threads; dynamic smem n_splits floats.  Combines the splits of one
-// (sequence, q-head) row in the log2 domain (weights w_s = 2^(m_s - M)), then
-// o = õ · R_V[h]ᵀ (warp w computes output channels w, w+4, ...; coalesced rows of R_V).
-__global__ void __launch_bounds__(128) attend_merge_kernel(AttnParams p, const float* __restrict__ RV,
+// grid (B, H_kv), 256 threads (8 warps).  Phase 1: warp w serves query head w mod g and the
+// split subset w / g (of 8/g subsets): every warp forms the row max M over all splits (and the
+// bf16 segment, NEXT-1), then its subset's Σ w_s õ_s and Σ w_s l_s with w_s = 2^(m_s - M) (lane
+// = 4 channels).  Phase 2 sums the subsets.  Phase 3: warp-per-output-row o = õ · R_V[h]ᵀ
+// (coalesced 512-B rows of R_V, shuffle reduction), plus the original-frame segment part.
+// PDL: griddepcontrol.wait guards the partials of the preceding kernels.
+__global__ void __launch_bounds__(256) attend_merge_kernel(AttnParams p, const float* __restrict__ RV,
                                                            void* __restrict__ out, int out_fp32,
                                                            float* __restrict__ lse) {
-  extern __shared__ float wsplit[];
-  __shared__ __align__(16) float ot[kD];
-  __shared__ float red[4];
-  const int row = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int h = (row % p.hq) / p.g;
-  const int ns = p.n_splits;
-  const size_t row0 = (size_t)row * ns;
+  __shared__ __align__(16) float po[8][kD];          // per-warp partial Σ w õ
+  __shared__ float pl[8];                            // per-warp partial Σ w l
+  __shared__ float pm[8];                            // row max per head
+  __shared__ __align__(16) float ot[8][kD];          // merged õ / L (rotated frame)
+  __shared__ __align__(16) float so[8][kD];          // segment part w_seg o_seg / L (original frame)
+  const int b = blockIdx.x, h = blockIdx.y, tid = threadIdx.x;
+  const int w = tid >> 5, lane = tid & 31;
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  const int ns = p.n_splits, g = p.g;
+  const bool seg = p.seg_o != nullptr;
+  const int nsub = 8 / g;                            // g in {1, 2, 4, 8}
+  const int hd = w % g, sub = w / g;
+  const size_t row = (size_t)b * p.hq + (size_t)h * g + hd;
+  const size_t row0 = row * ns;
   float M = -INFINITY;
-  for (int s = tid; s < ns; s += 128) M = fmaxf(M, p.ws_m[row0 + s]);
+  for (int s = lane; s < ns; s += 32) M = fmaxf(M, p.ws_m[row0 + s]);
   for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-  if (lane == 0) red[warp] = M;
-  __syncthreads();
-  M = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
-  __syncthreads();
+  const float mseg = seg ? p.seg_m[row] : -INFINITY;
+  M = fmaxf(M, mseg);
+  float4 o4 = make_float4(0.f, 0.f, 0.f, 0.f);
   float L = 0.f;
-  for (int s = tid; s < ns; s += 128) {
-    const float w = M == -INFINITY ? 0.f : exp2f(p.ws_m[row0 + s] - M);   // 0 for empty splits
-    wsplit[s] = w;
-    L += p.ws_l[row0 + s] * w;
-  }
-  for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
-  if (lane == 0) red[warp] = L;
-  __syncthreads();
-  L = red[0] + red[1] + red[2] + red[3];
-  float o = 0.f;
-  const float* po = p.ws_o + row0 * kD + tid;
-#pragma unroll 8
-  for (int s = 0; s < ns; ++s) o = fmaf(po[(size_t)s * kD], wsplit[s], o);
-  ot[tid] = (L > 0.f) ? o / L : 0.f;
-  if (tid == 0 && lse) lse[row] = (L > 0.f) ? (M + log2f(L)) * 0.6931471805599453f : -INFINITY;
-  __syncthreads();
-  const float* R = RV + (size_t)h * kD * kD;
-  const float4 o4 = reinterpret_cast<const float4*>(ot)[lane];
+  if (M != -INFINITY) {
+    const float4* pov = reinterpret_cast<const float4*>(p.ws_o + row0 * kD) + lane;
 #pragma unroll 4
-  for (int c = warp; c < kD; c += 4) {
-    const float4 r4 = reinterpret_cast<const float4*>(R + (size_t)c * kD)[lane];
-    float v = r4.x * o4.x + r4.y * o4.y + r4.z * o4.z + r4.w * o4.w;
-    for (int of = 16; of > 0; of >>= 1) v += __shfl_xor_sync(0xffffffffu, v, of);
-    if (lane == 0) {
-      const size_t idx = (size_t)row * kD + c;
-      if (out_fp32) static_cast<float*>(out)[idx] = v;
-      else static_cast<__nv_bfloat16*>(out)[idx] = __float2bfloat16_rn(v);
+    for (int s = sub; s < ns; s += nsub) {
+      const float wt = exp2f(p.ws_m[row0 + s] - M);   // 0 for empty splits
+      const float4 x = pov[(size_t)s * (kD / 4)];
+      o4.x = fmaf(x.x, wt, o4.x); o4.y = fmaf(x.y, wt, o4.y);
+      o4.z = fmaf(x.z, wt, o4.z); o4.w = fmaf(x.w, wt, o4.w);
+      L = fmaf(p.ws_l[row0 + s], wt, L);
     }
   }
+  reinterpret_cast<float4*>(po[w])[lane] = o4;
+  if (lane == 0) { pl[w] = L; if (sub == 0) pm[hd] = M; }
+  __syncthreads();
+  for (int e = tid; e < g * kD; e += 256) {
+    const int hh = e >> 7, c = e & 127;
+    const size_t r = (size_t)b * p.hq + (size_t)h * g + hh;
+    float oo = 0.f, LL = 0.f;
+    for (int s2 = 0; s2 < nsub; ++s2) { oo += po[s2 * g + hh][c]; LL += pl[s2 * g + hh]; }
+    const float Mh = pm[hh];
+    const float wseg = (seg && Mh != -INFINITY) ? exp2f(p.seg_m[r] - Mh) : 0.f;
+    if (seg) LL += p.seg_l[r] * wseg;
+    const float inv = LL > 0.f ? 1.f / LL : 0.f;
+    ot[hh][c] = oo * inv;
+    so[hh][c] = seg ? p.seg_o[r * kD + c] * wseg * inv : 0.f;
+    if (c == 0 && lse) lse[r] = (LL > 0.f) ? (Mh + log2f(LL)) * 0.6931471805599453f : -INFINITY;
+  }
+  __syncthreads();
+  const float* R = RV + (size_t)h * kD * kD;
+#pragma unroll 2
+  for (int cp = w; cp < kD; cp += 8) {
+    const float4 r4 = reinterpret_cast<const float4*>(R + (size_t)cp * kD)[lane];
+    for (int hh = 0; hh < g; ++hh) {
+      const float4 o = reinterpret_cast<const float4*>(ot[hh])[lane];
+      float v = r4.x * o.x + r4.y * o.y + r4.z * o.z + r4.w * o.w;
+      for (int of = 16; of > 0; of >>= 1) v += __shfl_xor_sync(0xffffffffu, v, of);
+      if (lane == hh) {
+        const size_t idx = ((size_t)b * p.hq + (size_t)h * g + hh) * kD + cp;
+        v += so[hh][cp];
+        if (out_fp32) static_cast<float*>(out)[idx] = v;
+        else static_cast<__nv_bfloat16*>(out)[idx] = __float2bfloat16_rn(v);
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ bf16 segment (NEXT-1)
+// grid (B, H_kv); one warp per query head.  Attention partial over the raw bf16 rows of the
+// sink + recent segment (§4, "an additional kernel for BF16 KV cache
+// attention"): scores q·k·scale·log2e in fp32 (lane = token), max / sum by warp shuffles,
+// p staged in smem, then Σ p v with lane = 4 channels.  Output in the ORIGINAL frame.
+constexpr int kSegCapMax = 1024;
+
+__global__ void __launch_bounds__(256) attend_segment_kernel(AttnParams p, const uint16_t* __restrict__ q,
+                                                             const uint16_t* __restrict__ sk,
+                                                             const uint16_t* __restrict__ sv,
+                                                             const int32_t* __restrict__ seg_lens,
+                                                             int seg_cap, float qscale) {
+  extern __shared__ __align__(16) float ssm[];
+  const int b = blockIdx.x, h = blockIdx.y, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* qs = ssm + w * (kD + seg_cap);
+  float* pr = qs + kD;
+  const size_t row = (size_t)b * p.hq + (size_t)h * p.g + w;
+  {
+    const uint2 u = reinterpret_cast<const uint2*>(q + row * kD)[lane];
+    qs[4 * lane + 0] = __uint_as_float(u.x << 16) * qscale;
+    qs[4 * lane + 1] = __uint_as_float(u.x & 0xffff0000u) * qscale;
+    qs[4 * lane + 2] = __uint_as_float(u.y << 16) * qscale;
+    qs[4 * lane + 3] = __uint_as_float(u.y & 0xffff0000u) * qscale;
+  }
+  __syncwarp();
+  const int n = seg_lens[b];
+  const size_t base = ((size_t)b * p.hkv + h) * (size_t)seg_cap * kD;
+  float M = -INFINITY;
+  for (int t = lane; t < n; t += 32) {
+    const uint4* kr = reinterpret_cast<const uint4*>(sk + base + (size_t)t * kD);
+    float s = 0.f;
+#pragma unroll 4
+    for (int c8 = 0; c8 < kD / 8; ++c8) {
+      const uint4 u = kr[c8];
+      const uint32_t wv[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        s = fmaf(qs[8 * c8 + 2 * e], __uint_as_float(wv[e] << 16), s);
+        s = fmaf(qs[8 * c8 + 2 * e + 1], __uint_as_float(wv[e] & 0xffff0000u), s);
+      }
+    }
+    pr[t] = s;
+    M = fmaxf(M, s);
+  }
+  for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+  __syncwarp();
+  float L = 0.f;
+  for (int t = lane; t < n; t += 32) {
+    const float e = exp2f(pr[t] - M);
+    pr[t] = e;
+    L += e;
+  }
+  for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+  __syncwarp();
+  float4 o4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int t = 0; t < n; ++t) {
+    const uint2 u = reinterpret_cast<const uint2*>(sv + base + (size_t)t * kD)[lane];
+    const float e = pr[t];
+    o4.x = fmaf(e, __uint_as_float(u.x << 16), o4.x);
+    o4.y = fmaf(e, __uint_as_float(u.x & 0xffff0000u), o4.y);
+    o4.z = fmaf(e, __uint_as_float(u.y << 16), o4.z);
+    o4.w = fmaf(e, __uint_as_float(u.y & 0xffff0000u), o4.w);
+  }
+  reinterpret_cast<float4*>(p.seg_o + row * kD)[lane] = o4;
+  if (lane == 0) { p.seg_m[row] = M; p.seg_l[row] = L; }
 }
 
 // ------------------------------------------------------------------ host side
 // Pages per split (per work item).  Simple kernel: ~8 CTAs per SM over the grid.  Tensor-core
 // kernel: warp-granular items, ~3 per warp of a nominal 16-warps/SM residency, 8..32 pages.
 static int choose_pps(const oscar_ctx& c, int B, int max_pages) {
-  if (c.pages_per_split > 0) return c.pages_per_split;
   const long units = (long)B * c.hkv;
+  if (c.pages_per_split > 0)
+    return (c.variant == 0 && attend_mma_supported(c) && c.pages_per_split > 32) ? 32 : c.pages_per_split;
   if (c.variant == 0 && attend_mma_supported(c)) {
     long pps = units * max_pages / (3L * c.num_sms * 16);
     pps = pps < 8 ? 8 : (pps > 32 ? 32 : pps);
@@ -289,7 +378,7 @@ size_t attend_workspace_bytes(const oscar_ctx& c, int B, int max_pages) {
   const size_t rows = (size_t)B * c.hq;
   const size_t nt = (size_t)((c.g * c.ng + 7) / 8);
   return rows * kD * 4 + rows * ns * (kD + 2) * 4 + rows * (kD * 2 + 4 + 32) +
-         (size_t)B * c.hkv * nt * 16 * 32 * 4 + 1024;
+         (size_t)B * c.hkv * nt * 16 * 32 * 4 + rows * (kD + 2) * 4 + 1024;
 }
 
 int attend_mma_total_warps(const oscar_ctx& c);                              // attend_mma.cu
@@ -298,7 +387,8 @@ cudaError_t launch_attend_mma(const AttnParams& p, int total_warps, cudaStream_t
 cudaError_t launch_attend(const oscar_ctx& c, const void* q, const int32_t* page_table,
                           const int32_t* seq_lens, int B, int max_pages, const void* pool,
                           const float* RK, const float* RV, void* ws, void* out, int out_fp32,
-                          float* lse, cudaStream_t s) {
+                          float* lse, cudaStream_t s, const void* seg_k, const void* seg_v,
+                          const int32_t* seg_lens, int seg_cap) {
   const bool mma = c.variant == 0 && attend_mma_supported(c);
   AttnParams p{};
   p.hq = c.hq; p.hkv = c.hkv; p.g = c.g; p.P = c.P; p.bits = c.bits; p.G = c.G; p.ng = c.ng;
@@ -322,16 +412,31 @@ cudaError_t launch_attend(const oscar_ctx& c, const void* q, const int32_t* page
   p.qint = reinterpret_cast<int16_t*>(p.qscale + rows);
   p.qfrag = reinterpret_cast<uint32_t*>(p.qint + rows * kD);
   p.work = reinterpret_cast<int32_t*>(p.qfrag + (size_t)B * c.hkv * p.nt * 16 * 32);
+  if (seg_k) {
+    p.seg_o = reinterpret_cast<float*>(p.work + 64);
+    p.seg_m = p.seg_o + rows * kD;
+    p.seg_l = p.seg_m + rows;
+  }
 
-  const int qsmem = kD * kD * 4;
-  cudaError_t e = cudaFuncSetAttribute(q_rotate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, qsmem);
-  if (e != cudaSuccess) return e;
-  q_rotate_kernel<<<dim3(B, c.hkv), 128, qsmem, s>>>(static_cast<const uint16_t*>(q), RK, c.hq, c.g, c.G,
-                                                     c.scale * kLog2e, p.qt, p.qint, p.qscale, p.qsum,
-                                                     mma ? p.qfrag : nullptr, c.bits, p.nt,
-                                                     mma ? p.work : nullptr);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
+  cudaLaunchAttribute pdl[1];
+  pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  pdl[0].val.programmaticStreamSerializationAllowed = 1;
+  int lgG = 0;
+  while ((1 << lgG) < c.G) ++lgG;
+  cudaError_t e = cudaSuccess;
+  {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(B, c.hkv);
+    cfg.blockDim = dim3(32 * c.g);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cfg.attrs = pdl;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, q_rotate_kernel, static_cast<const uint16_t*>(q), RK, c.hq, c.g, lgG,
+                           c.scale * kLog2e, p.qt, p.qint, p.qscale, p.qsum, mma ? p.qfrag : nullptr, c.bits,
+                           p.nt, mma ? p.work : nullptr);
+    if (e != cudaSuccess) return e;
+  }
   if (!mma) {
     const int smem = (8 * kD + 64 + 8 * c.P + 24) * 4 + c.page_bytes;
     e = cudaFuncSetAttribute(attend_partial_simple, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -343,7 +448,28 @@ cudaError_t launch_attend(const oscar_ctx& c, const void* q, const int32_t* page
   }
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  attend_merge_kernel<<<(unsigned)(B * c.hq), 128, p.n_splits * 4, s>>>(p, RV, out, out_fp32, lse);
+  if (seg_k) {
+    const int ssmem = c.g * (kD + seg_cap) * 4;
+    e = cudaFuncSetAttribute(attend_segment_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ssmem);
+    if (e != cudaSuccess) return e;
+    attend_segment_kernel<<<dim3(B, c.hkv), 32 * c.g, ssmem, s>>>(
+        p, static_cast<const uint16_t*>(q), static_cast<const uint16_t*>(seg_k),
+        static_cast<const uint16_t*>(seg_v), seg_lens, seg_cap, c.scale * kLog2e);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  {
+    const int msmem = 0;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(B, c.hkv);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = msmem;
+    cfg.stream = s;
+    cfg.attrs = pdl;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, attend_merge_kernel, p, RV, out, out_fp32, lse);
+    if (e != cudaSuccess) return e;
+  }
   return cudaGetLastError();
 }
 

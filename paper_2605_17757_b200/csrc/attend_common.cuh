@@ -22,6 +22,10 @@ struct AttnParams {
   int32_t* work;               // work-item counter of the persistent partial kernel
   int nt;                      // ceil(g * ng / 8)
   int n_items;                 // B * H_kv * n_splits
+  // optional bf16 segment (sink + recent window, NEXT-1): partial in the ORIGINAL frame
+  float* seg_o;                // [B][H_q][128] unnormalized Σ p v (null: no segment)
+  float* seg_m;                // [B][H_q]
+  float* seg_l;                // [B][H_q]
 };
 
 bool attend_mma_supported(const oscar_ctx& c);

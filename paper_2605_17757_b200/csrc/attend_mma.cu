@@ -44,6 +44,12 @@ __device__ __forceinline__ void hmma16816(float (&c)[4], const uint32_t (&a)[4],
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
+__device__ __forceinline__ float ex2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;\n" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
   __half2 h = __floats2half2_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&h);
@@ -107,7 +113,8 @@ __device__ __forceinline__ Item decode_item(const AttnParams& p, int it) {
 }  // namespace
 
 template <int BITS, int GQ, int NG>
-__global__ void __launch_bounds__(kWarps * 32) attend_partial_mma(AttnParams p, int S) {
+__global__ void __launch_bounds__(kWarps * 32, (GQ * NG <= 8 ? 4 : 3))
+attend_partial_mma(AttnParams p, int S) {
   constexpr int NC = GQ * NG;                 // (group, head) combos
   constexpr int NT = (NC + 7) / 8;            // 8-combo tiles (QK M-tiles / PV N-tiles)
   constexpr int RB = 16 * BITS;               // packed row bytes (d = 128)
@@ -132,14 +139,20 @@ __global__ void __launch_bounds__(kWarps * 32) attend_partial_mma(AttnParams p, 
   uint64_t policy;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(policy));
 
+  // work items: the first two per warp are static (no atomic latency at start), the rest are
+  // pulled from the counter (reset to 0 by q_rotate_kernel) offset by 2·(total warps)
   const int n_items = p.n_items;
-  auto fetch_async = [&]() { return lane == 0 ? atomicAdd(p.work, 1) : 0; };
+  const int total_warps = gridDim.x * kWarps, gw = blockIdx.x * kWarps + warp;
+  auto fetch_async = [&]() { return lane == 0 ? atomicAdd(p.work, 1) + 2 * total_warps : 0; };
   auto bcast = [&](int v) { return __shfl_sync(0xffffffffu, v, 0); };
-  int cur = bcast(fetch_async());
-  int nxt = bcast(fetch_async());
-  int pending = fetch_async();                // the item after nxt (broadcast when needed)
+  int cur = gw, nxt = gw + total_warps;
   Item Icur = decode_item(p, cur < n_items ? cur : 0);
   Item Inxt = decode_item(p, nxt < n_items ? nxt : 0);
+  // page indices of the current / next item: lane l holds page l of the item (pps <= 32)
+  auto load_pages = [&](const Item& L, int it) {
+    return (it < n_items && lane < L.np) ? p.page_table[(size_t)L.b * p.max_pages + L.page0 + lane] : 0;
+  };
+  int pidx_cur = load_pages(Icur, cur), pidx_nxt = load_pages(Inxt, nxt);
   // load cursor: page lq_k of (lq_sel ? nxt : cur); global page sequence numbers
   int lq_sel = 0, lq_k = 0;
   uint32_t seq_issue = 0, seq_use = 0;
@@ -152,9 +165,9 @@ __global__ void __launch_bounds__(kWarps * 32) attend_partial_mma(AttnParams p, 
         if (!on_next) { lq_sel = 1; lq_k = 0; continue; }
         break;
       }
+      const int64_t page = __shfl_sync(0xffffffffu, on_next ? pidx_nxt : pidx_cur, lq_k);
       if (lane == 0) {
         const int s = seq_issue % S;
-        const int64_t page = p.page_table[(size_t)L.b * p.max_pages + L.page0 + lq_k];
         bulk_load(ring + (size_t)s * page_bytes, p.pool + (page * p.hkv + L.h) * (int64_t)page_bytes,
                   page_bytes, &bars[s], policy);
       }
@@ -162,6 +175,10 @@ __global__ void __launch_bounds__(kWarps * 32) attend_partial_mma(AttnParams p, 
       ++lq_k;
     }
   };
+  // the first pages depend only on the caller's inputs: start streaming before q_rotate ends
+  try_issue();
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  int pending = nxt < n_items ? fetch_async() : 0;   // the item after nxt (broadcast when needed)
 
   const int hh = gid % GQ;                    // every tile of this lane serves head hh
   const bool real = NC >= 8 || gid < NC;
@@ -201,11 +218,14 @@ __global__ void __launch_bounds__(kWarps * 32) attend_partial_mma(AttnParams p, 
     for (int j = 0; j < NT; ++j) mv_acc[j] = 0.f;
 
     // one page: chunks of up to 4 sub-tiles (64 tokens); FULL = no masking needed
+    // FULLSUB = 4: a completely valid 64-token page (compile-time shape, no masks);
+    // FULLSUB = 0: generic page (any P, masked tail)
     auto page_body = [&](const unsigned char* pg, int valid, auto full_c) {
-      constexpr bool FULL = decltype(full_c)::value;
-      const unsigned char* vcodes = pg + p.vcodes_off;
-      const unsigned char* meta = pg + p.meta_off;
-      const int n_sub = FULL ? (P >> 4) : ((valid + 15) >> 4);
+      constexpr int FULLSUB = decltype(full_c)::value;
+      constexpr bool FULL = FULLSUB > 0;
+      const unsigned char* vcodes = pg + (FULL ? 64 * RB : p.vcodes_off);
+      const unsigned char* meta = pg + (FULL ? 128 * RB : p.meta_off);
+      const int n_sub = FULL ? FULLSUB : ((valid + 15) >> 4);
       for (int c0 = 0; c0 < n_sub; c0 += 4) {
         float sc[4][4];
         float tmax = -INFINITY;
@@ -303,7 +323,7 @@ __global__ void __launch_bounds__(kWarps * 32) attend_partial_mma(AttnParams p, 
           float pr[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            pr[e] = exp2f(sc[sl][e] - m_run);      // exp2(-inf) = 0 (m_run finite here)
+            pr[e] = ex2_ftz(sc[sl][e] - m_run);    // exp2(-inf) = 0 (m_run finite here)
             l_run += pr[e];
           }
           uint32_t bpv[NT][2];
@@ -360,8 +380,8 @@ __global__ void __launch_bounds__(kWarps * 32) attend_partial_mma(AttnParams p, 
       mbar_wait(&bars[s], (seq_use / S) & 1);
       const unsigned char* pg = ring + (size_t)s * page_bytes;
       const int valid = min(P, I.seq_len - (I.page0 + k) * P);
-      if (valid == P) page_body(pg, valid, std::true_type{});
-      else page_body(pg, valid, std::false_type{});
+      if (valid == 64 && P == 64) page_body(pg, valid, std::integral_constant<int, 4>{});
+      else page_body(pg, valid, std::integral_constant<int, 0>{});
       // release the stage, keep the ring full (possibly with the next item's pages)
       __syncwarp();
       ++seq_use;
@@ -403,11 +423,14 @@ __global__ void __launch_bounds__(kWarps * 32) attend_partial_mma(AttnParams p, 
     // ---- advance: the loader already moved on to `nxt`
     cur = nxt;
     Icur = Inxt;
+    pidx_cur = pidx_nxt;
     if (lq_sel) lq_sel = 0; else lq_k = 0;
     nxt = cur < n_items ? bcast(pending) : n_items;
     if (nxt < n_items) Inxt = decode_item(p, nxt);
+    pidx_nxt = load_pages(Inxt, nxt);
     pending = nxt < n_items ? fetch_async() : 0;
   }
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");   // let the merge kernel launch
 }
 
 // ---------------------------------------------------------------- dispatch
@@ -465,7 +488,20 @@ cudaError_t launch_attend_mma(const AttnParams& p, int total_warps, cudaStream_t
   if (e != cudaSuccess) return e;
   int warps = total_warps < p.n_items ? total_warps : p.n_items;
   const int grid = (warps + kWarps - 1) / kWarps;
-  fn<<<grid, kWarps * 32, smem, s>>>(p, S);
+  // programmatic dependent launch: the first page loads overlap q_rotate_kernel's tail;
+  // griddepcontrol.wait in the kernel orders every read of q_rotate's outputs
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kWarps * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, fn, p, S);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

@@ -185,7 +185,8 @@ def test_attend_parity(cfg, variant, pps):
     lg = lse.cpu().numpy()
     fin = np.isfinite(ref_lse)
     assert np.array_equal(np.isfinite(lg), fin)
-    assert np.abs(lg[fin] - ref_lse[fin]).max() <= 1e-3
+    # lse: the IMMA path quantizes q̃ to 15 bits (reading Z31): logit error <= ~1e-4 relative
+    assert (np.abs(lg[fin] - ref_lse[fin]) <= 1e-3 + 1e-4 * np.abs(ref_lse[fin])).all()
 
 
 def test_attend_page_indirection_invariance():
@@ -234,13 +235,14 @@ def test_attend_full_size_sampled():
 
 
 # ---------------------------------------------------------------------------- calibration
-def test_calibration_parity_by_invariants():
+@pytest.mark.parametrize("variant,N,Hq,Hkv", [(0, 3000, 8, 2), (1, 3000, 8, 2), (0, 2500, 16, 2), (0, 9000, 2, 2)])
+def test_calibration_parity_by_invariants(variant, N, Hq, Hkv):
     torch = _torch()
-    rng = np.random.default_rng(21)
-    N, Hq, Hkv = 3000, 8, 2
+    rng = np.random.default_rng(21 + N + Hq)
     Q = synth.gen_queries(rng, N, Hq, Hkv, 128)
     SV = synth.gen_sv(rng, N, Hq, 128)
     o = make(num_q_heads=Hq, num_kv_heads=Hkv)
+    o.set_variant(variant)
     acc = torch.zeros((Hkv, 2, 128, 128), dtype=torch.float64, device="cuda")
     o.calib_accumulate(T(Q[:1234], torch.bfloat16), T(SV[:1234], torch.bfloat16), acc)
     o.calib_accumulate(T(Q[1234:], torch.bfloat16), T(SV[1234:], torch.bfloat16), acc)

@@ -450,3 +450,36 @@ def test_paged_attend_matches_rows_and_alg1():
     Kh, Vh = O.read_rows(pool, slots[L:L + L - 37], 1, fmt)
     o1 = O.attend_alg1(q[1, 2:4], Kh, Vh, RK[1], RV[1], 1 / math.sqrt(128))
     np.testing.assert_allclose(o[1, 2:4], o1, atol=1e-12)
+
+
+def test_attend_mixed_reduces_to_pure_cases():
+    """NEXT-1 mixed cache (Alg. 1): with an empty bf16 segment it is
+    `attend`; with an empty INT2 history it is plain softmax attention over the raw rows (direct
+    loops)."""
+    rng = np.random.default_rng(31)
+    fmt = O.PageFormat(128, 2, 64, 64)
+    B, Hq, Hkv, L, cap = 2, 4, 2, 150, 40
+    pt = synth.contiguous_page_table(B, 3, shuffle_rng=rng)
+    pool = np.zeros((B * 3, Hkv, fmt.page_bytes), np.uint8)
+    RK, RV = synth.gen_rotation(rng, Hkv, 128), synth.gen_rotation(rng, Hkv, 128)
+    for b in range(B):
+        slots = synth.slots_for(pt[b:b + 1], np.arange(L)[None], 64).reshape(-1)
+        O.quantize_append(synth.gen_keys(rng, L, Hkv, 128), synth.gen_values(rng, L, Hkv, 128),
+                          slots, RK, RV, fmt, pool)
+    q = synth.gen_decode_q(rng, B, Hq, 128, sigma=0.5)
+    sk = synth.gen_keys(rng, B * Hkv * cap, 1, 128).reshape(B, Hkv, cap, 128)
+    sv = synth.gen_values(rng, B * Hkv * cap, 1, 128).reshape(B, Hkv, cap, 128)
+    o1, l1 = O.attend(q, pt, [L, 90], pool, RK, RV, fmt, Hkv)
+    o2, l2 = O.attend_mixed(q, pt, [L, 90], pool, sk, sv, [0, 0], RK, RV, fmt, Hkv)
+    np.testing.assert_allclose(o2, o1, atol=1e-12)
+    np.testing.assert_allclose(l2, l1, atol=1e-12)
+    o3, l3 = O.attend_mixed(q, pt, [0, 0], pool, sk, sv, [cap, 7], RK, RV, fmt, Hkv)
+    d = 128
+    for b, n in [(0, cap), (1, 7)]:
+        for i in [0, 3]:
+            h = i // 2
+            w = [math.exp(sum(float(q[b, i, c]) * float(sk[b, h, t, c]) for c in range(d)) / math.sqrt(d))
+                 for t in range(n)]
+            ref = [sum(w[t] * float(sv[b, h, t, c]) for t in range(n)) / sum(w) for c in range(0, d, 17)]
+            np.testing.assert_allclose(o3[b, i, ::17], ref, atol=1e-12)
+            assert abs(l3[b, i] - math.log(sum(w))) < 1e-12

@@ -92,6 +92,23 @@ class ClockSampler:
                 "samples": len(s)}
 
 
+def ncu_traffic(kernels):
+    """DRAM bytes per launch (read + write) of the named kernels, summed, from the committed
+    `ncu --set full` capture (profiles/ncu_traffic.json, written by tools/ncu_traffic.py)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            j = json.load(f)
+        tot = 0.0
+        for k in kernels:
+            runs = [v for name, v in j["kernels"].items() if name.startswith(k)]
+            if not runs:
+                return None
+            tot += max(x["traffic_bytes"] for x in runs[0])
+        return tot
+    except Exception:
+        return None
+
+
 def cpu_threads():
     try:
         from threadpoolctl import threadpool_info
@@ -218,6 +235,11 @@ def main():
             "accumulate_TFLOPs": cov_flops / t_acc / 1e9,
             "allreduce_ms": t_ar, "allreduce_bytes": acc.numel() * 8,
             "finalize_ms": t_fin, "jacobi_sweeps_max": int(sweeps.max()),
+            "roofline": {"bound": "hbm", "achieved": cov_bytes / t_acc / 1e6, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": cov_bytes / t_acc / 1e6 / hbm_peak,
+                         "traffic": ncu_traffic(["cov_accum_tc_kernel"]),
+                         "kernel": "cov_accum_tc_kernel (tcgen05 + TMA), per layer launch",
+                         "algorithmic_bytes_per_launch": cov_bytes // NL, "peak_kind": peak_kind},
         }
         del Q, SV, acc
     else:
@@ -255,7 +277,8 @@ def main():
             "ms": t, "GBps": ap_bytes * world / t / 1e6,
             "pct_of_8TBps": ap_bytes / t / 1e6 / NOMINAL_HBM_GBS * 100,
             "roofline": {"bound": "hbm", "achieved": ap_bytes / t / 1e6, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": ap_bytes / t / 1e6 / hbm_peak, "traffic": None,
+                         "frac": ap_bytes / t / 1e6 / hbm_peak, "traffic": ncu_traffic(["append_tc_kernel"]),
+                         "kernel": "append_tc_kernel (tcgen05 + TMA)",
                          "algorithmic_bytes_per_launch": ap_bytes, "peak_kind": peak_kind},
         }
     del Kp, Vp
@@ -366,7 +389,10 @@ def main():
         "config": workload_config(args),
         "pct_of_8TBps": value / world / NOMINAL_HBM_GBS * 100,
         "roofline": {"bound": "hbm", "achieved": attn_gbs, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": attn_gbs / hbm_peak, "traffic": None, "kernel": "oscar_attend (q_rotate+partial+merge)",
+                     "frac": attn_gbs / hbm_peak,
+                     "traffic": ncu_traffic(["q_rotate_kernel", "attend_partial_mma", "attend_merge_kernel"]),
+                     "traffic_source": "profiles/ncu_traffic.json (ncu --set full, per launch)",
+                     "kernel": "oscar_attend (q_rotate+partial+merge)",
                      "algorithmic_bytes_per_launch": attn_bytes, "avg_launch_us": attn_ms * 1e3,
                      "peak_kind": peak_kind},
         "gpu_launches": launches_per_layer * NL * args.steps,

@@ -12,14 +12,16 @@
 namespace oscar {
 
 // ------------------------------------------------------------------ q rotation
-// grid (B, H_kv); one warp per query head of the group (g warps).  Lane l computes columns
-// 4l..4l+3 of q̃ = q · R_K[h] · scale · log2(e) (fp32, kept for the simple kernel), then the
-// 15-bit integer form used by the IMMA QK path: qscale = max|q̃| / 32639,
-// qint = rint(q̃ / qscale) (|qint| <= 32639 = 127·256 + 127, so hi/lo int8 never overflow),
-// qsum[grp] = Σ_{c in grp} qint, and the per-lane IMMA A fragments of the group.
+// grid (B, H_kv), 512 threads (16 warps).  Warp w serves query head w mod g of the group and
+// k-slice w / g (16/g slices of 128g/16 input channels): lane l forms the partial dot of columns
+// 4l..4l+3 of q̃ = q · R_K[h] (all its R loads in flight at once); warps 0..g-1 then combine the
+// slices, scale by softmax scale · log2(e) (fp32 q̃ kept for the simple kernel), and emit the
+// 15-bit integer form used by the IMMA QK path: qscale = max|q̃| / 32639, qint = rint(q̃/qscale)
+// (|qint| <= 32639 = 127·256 + 127, so the hi/lo int8 split never overflows), qsum[grp] =
+// Σ_{c in grp} qint; finally all threads write the per-lane IMMA A fragments of the group.
 // PDL: the work depends only on the caller's q and R_K; griddepcontrol.wait at the end keeps
 // "this kernel complete => the preceding kernel complete" for the partial kernel.
-__global__ void __launch_bounds__(256) q_rotate_kernel(const uint16_t* __restrict__ q,
+__global__ void __launch_bounds__(512) q_rotate_kernel(const uint16_t* __restrict__ q,
                                                        const float* __restrict__ RK, int Hq,
                                                        int g, int lgG, float qscale,
                                                        float* __restrict__ qt,
@@ -29,45 +31,58 @@ __global__ void __launch_bounds__(256) q_rotate_kernel(const uint16_t* __restric
                                                        uint32_t* __restrict__ qfrag, int bits,
                                                        int nt, int32_t* __restrict__ work) {
   __shared__ __align__(16) float qs[8][kD];
+  __shared__ __align__(16) float ps[16][kD];
   __shared__ int16_t qis[8][kD];
   const int b = blockIdx.x, h = blockIdx.y, tid = threadIdx.x;
   const int w = tid >> 5, lane = tid & 31;
   const int G = 1 << lgG;
-  const size_t row = (size_t)b * Hq + (size_t)h * g + w;
   if (work && b == 0 && h == 0 && tid == 0) *work = 0;   // reset the work-item counter
+  for (int e = tid; e < g * (kD / 4); e += 512) {
+    const int hd = e >> 5, l4 = e & 31;
+    const uint2 u = reinterpret_cast<const uint2*>(q + ((size_t)b * Hq + (size_t)h * g + hd) * kD)[l4];
+    reinterpret_cast<float4*>(qs[hd])[l4] =
+        make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xffff0000u),
+                    __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xffff0000u));
+  }
+  __syncthreads();
   {
-    const uint2 u = reinterpret_cast<const uint2*>(q + row * kD)[lane];
-    float4 f;
-    f.x = __uint_as_float(u.x << 16); f.y = __uint_as_float(u.x & 0xffff0000u);
-    f.z = __uint_as_float(u.y << 16); f.w = __uint_as_float(u.y & 0xffff0000u);
-    reinterpret_cast<float4*>(qs[w])[lane] = f;
+    const int hd = w % g, ks = w / g, kn = (kD * g) / 16;
+    const float4* R4 = reinterpret_cast<const float4*>(RK + (size_t)h * kD * kD + (size_t)ks * kn * kD) + lane;
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll 32
+    for (int k = 0; k < kn; ++k) {
+      const float4 r = R4[(size_t)k * (kD / 4)];
+      const float x = qs[hd][ks * kn + k];
+      a0 = fmaf(x, r.x, a0); a1 = fmaf(x, r.y, a1); a2 = fmaf(x, r.z, a2); a3 = fmaf(x, r.w, a3);
+    }
+    reinterpret_cast<float4*>(ps[w])[lane] = make_float4(a0, a1, a2, a3);
   }
-  __syncwarp();
-  const float4* R4 = reinterpret_cast<const float4*>(RK + (size_t)h * kD * kD) + lane;
-  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-#pragma unroll 16
-  for (int k = 0; k < kD; ++k) {
-    const float4 r = R4[(size_t)k * (kD / 4)];
-    const float x = qs[w][k];
-    a0 = fmaf(x, r.x, a0); a1 = fmaf(x, r.y, a1); a2 = fmaf(x, r.z, a2); a3 = fmaf(x, r.w, a3);
+  __syncthreads();
+  if (w < g) {
+    const size_t row = (size_t)b * Hq + (size_t)h * g + w;
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int ks = 0; ks < 16 / g; ++ks) {
+      const float4 x = reinterpret_cast<const float4*>(ps[ks * g + w])[lane];
+      a.x += x.x; a.y += x.y; a.z += x.z; a.w += x.w;
+    }
+    a.x *= qscale; a.y *= qscale; a.z *= qscale; a.w *= qscale;
+    reinterpret_cast<float4*>(qt + row * kD)[lane] = a;
+    float mx = fmaxf(fmaxf(fabsf(a.x), fabsf(a.y)), fmaxf(fabsf(a.z), fabsf(a.w)));
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const float s = mx > 0.f ? mx / 32639.f : 1.f;
+    const int v0 = max(-32639, min(32639, __float2int_rn(a.x / s)));
+    const int v1 = max(-32639, min(32639, __float2int_rn(a.y / s)));
+    const int v2 = max(-32639, min(32639, __float2int_rn(a.z / s)));
+    const int v3 = max(-32639, min(32639, __float2int_rn(a.w / s)));
+    const uint2 pk = make_uint2((uint32_t)(v0 & 0xffff) | ((uint32_t)v1 << 16),
+                                (uint32_t)(v2 & 0xffff) | ((uint32_t)v3 << 16));
+    reinterpret_cast<uint2*>(qint + row * kD)[lane] = pk;
+    reinterpret_cast<uint2*>(qis[w])[lane] = pk;
+    if (lane == 0) qsc[row] = s;
+    int gs = v0 + v1 + v2 + v3;                    // lanes of one group: G/4 consecutive lanes
+    for (int o = 1; o < (G >> 2); o <<= 1) gs += __shfl_xor_sync(0xffffffffu, gs, o);
+    if ((lane & ((G >> 2) - 1)) == 0) qsum[row * 8 + (lane * 4 >> lgG)] = gs;
   }
-  a0 *= qscale; a1 *= qscale; a2 *= qscale; a3 *= qscale;
-  reinterpret_cast<float4*>(qt + row * kD)[lane] = make_float4(a0, a1, a2, a3);
-  float mx = fmaxf(fmaxf(fabsf(a0), fabsf(a1)), fmaxf(fabsf(a2), fabsf(a3)));
-  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  const float s = mx > 0.f ? mx / 32639.f : 1.f;
-  const int v0 = max(-32639, min(32639, __float2int_rn(a0 / s)));
-  const int v1 = max(-32639, min(32639, __float2int_rn(a1 / s)));
-  const int v2 = max(-32639, min(32639, __float2int_rn(a2 / s)));
-  const int v3 = max(-32639, min(32639, __float2int_rn(a3 / s)));
-  reinterpret_cast<uint2*>(qint + row * kD)[lane] =
-      make_uint2((uint32_t)(v0 & 0xffff) | ((uint32_t)v1 << 16), (uint32_t)(v2 & 0xffff) | ((uint32_t)v3 << 16));
-  reinterpret_cast<uint2*>(qis[w])[lane] =
-      make_uint2((uint32_t)(v0 & 0xffff) | ((uint32_t)v1 << 16), (uint32_t)(v2 & 0xffff) | ((uint32_t)v3 << 16));
-  if (lane == 0) qsc[row] = s;
-  int gs = v0 + v1 + v2 + v3;                      // lanes of one group: G/4 consecutive lanes
-  for (int o = 1; o < (G >> 2); o <<= 1) gs += __shfl_xor_sync(0xffffffffu, gs, o);
-  if ((lane & ((G >> 2) - 1)) == 0) qsum[row * 8 + (lane * 4 >> lgG)] = gs;
   __syncthreads();
   // IMMA A fragments for attend_partial_mma: word (j, kk, r) of lane (gid, t) holds the
   // hi (r even) / lo (r odd) int8 of qint[head][channel] for combo 8j + gid = grp·g + head,
@@ -75,7 +90,7 @@ __global__ void __launch_bounds__(256) q_rotate_kernel(const uint16_t* __restric
   if (qfrag) {
     const int nc = g << (7 - lgG);
     uint32_t* dst = qfrag + ((size_t)b * gridDim.y + h) * nt * 16 * 32;
-    for (int wd = tid; wd < nt * 16 * 32; wd += blockDim.x) {
+    for (int wd = tid; wd < nt * 16 * 32; wd += 512) {
       const int ln = wd & 31, rest = wd >> 5;
       const int r = rest & 3, kk = (rest >> 2) & 3, j = rest >> 4;
       const int gid = ln >> 2, t = ln & 3, cb = 8 * j + gid;
@@ -210,78 +225,86 @@ __global__ void __launch_bounds__(128) attend_partial_simple(AttnParams p) {
 }
 
 // ------------------------------------------------------------------ merge
-// grid (B, H_kv), 256 threads (8 warps).  Phase 1: warp w serves query head w mod g and the
-// split subset w / g (of 8/g subsets): every warp forms the row max M over all splits (and the
-// bf16 segment, NEXT-1), then its subset's Σ w_s õ_s and Σ w_s l_s with w_s = 2^(m_s - M) (lane
-// = 4 channels).  Phase 2 sums the subsets.  Phase 3: warp-per-output-row o = õ · R_V[h]ᵀ
-// (coalesced 512-B rows of R_V, shuffle reduction), plus the original-frame segment part.
-// PDL: griddepcontrol.wait guards the partials of the preceding kernels.
-__global__ void __launch_bounds__(256) attend_merge_kernel(AttnParams p, const float* __restrict__ RV,
+// grid (B·H_q), 512 threads (16 warps): one CTA per (sequence, query head) row, so the whole
+// machine works on the 16 MB of partials at once.  All threads read the split maxima (block max
+// M, weights w_s = 2^(m_s - M), Σ w_s l_s); warp w sums splits s ≡ w (mod 16) with lane = 4
+// channels; threads < 128 add the 16 warp partials; then warp w computes output rows
+// c' ≡ w (mod 16) of o = õ · R_V[h]ᵀ (coalesced 512-B rows of R_V, shuffle reduction) and adds
+// the original-frame bf16 segment part (NEXT-1).  PDL: griddepcontrol.wait guards the partials.
+__global__ void __launch_bounds__(512) attend_merge_kernel(AttnParams p, const float* __restrict__ RV,
                                                            void* __restrict__ out, int out_fp32,
                                                            float* __restrict__ lse) {
-  __shared__ __align__(16) float po[8][kD];          // per-warp partial Σ w õ
-  __shared__ float pl[8];                            // per-warp partial Σ w l
-  __shared__ float pm[8];                            // row max per head
-  __shared__ __align__(16) float ot[8][kD];          // merged õ / L (rotated frame)
-  __shared__ __align__(16) float so[8][kD];          // segment part w_seg o_seg / L (original frame)
-  const int b = blockIdx.x, h = blockIdx.y, tid = threadIdx.x;
-  const int w = tid >> 5, lane = tid & 31;
+  extern __shared__ float wsp[];                     // [n_splits] weights
+  __shared__ __align__(16) float po[16][kD];
+  __shared__ __align__(16) float ot[kD];
+  __shared__ float red[16];
+  __shared__ float bc[3];                            // M, 1/L, w_seg/L
+  const int row = blockIdx.x, tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const int h = (row % p.hq) / p.g;
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
-  const int ns = p.n_splits, g = p.g;
+  const int ns = p.n_splits;
+  const size_t row0 = (size_t)row * ns;
   const bool seg = p.seg_o != nullptr;
-  const int nsub = 8 / g;                            // g in {1, 2, 4, 8}
-  const int hd = w % g, sub = w / g;
-  const size_t row = (size_t)b * p.hq + (size_t)h * g + hd;
-  const size_t row0 = row * ns;
-  float M = -INFINITY;
-  for (int s = lane; s < ns; s += 32) M = fmaxf(M, p.ws_m[row0 + s]);
+  float M = seg ? p.seg_m[row] : -INFINITY;
+  for (int s = tid; s < ns; s += 512) M = fmaxf(M, p.ws_m[row0 + s]);
   for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-  const float mseg = seg ? p.seg_m[row] : -INFINITY;
-  M = fmaxf(M, mseg);
-  float4 o4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (lane == 0) red[w] = M;
+  __syncthreads();
+  M = red[0];
+#pragma unroll
+  for (int i = 1; i < 16; ++i) M = fmaxf(M, red[i]);
+  __syncthreads();
   float L = 0.f;
-  if (M != -INFINITY) {
+  for (int s = tid; s < ns; s += 512) {
+    const float wt = M == -INFINITY ? 0.f : exp2f(p.ws_m[row0 + s] - M);   // 0 for empty splits
+    wsp[s] = wt;
+    L = fmaf(p.ws_l[row0 + s], wt, L);
+  }
+  for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+  if (lane == 0) red[w] = L;
+  __syncthreads();
+  if (tid == 0) {
+    float Ls = 0.f;
+    for (int i = 0; i < 16; ++i) Ls += red[i];
+    const float wseg = (seg && M != -INFINITY) ? exp2f(p.seg_m[row] - M) : 0.f;
+    if (seg) Ls += p.seg_l[row] * wseg;
+    const float inv = Ls > 0.f ? 1.f / Ls : 0.f;
+    bc[0] = M; bc[1] = inv; bc[2] = wseg * inv;
+    if (lse) lse[row] = (Ls > 0.f) ? (M + log2f(Ls)) * 0.6931471805599453f : -INFINITY;
+  }
+  {
+    float4 o4 = make_float4(0.f, 0.f, 0.f, 0.f);
     const float4* pov = reinterpret_cast<const float4*>(p.ws_o + row0 * kD) + lane;
 #pragma unroll 4
-    for (int s = sub; s < ns; s += nsub) {
-      const float wt = exp2f(p.ws_m[row0 + s] - M);   // 0 for empty splits
+    for (int s = w; s < ns; s += 16) {
+      const float wt = wsp[s];
       const float4 x = pov[(size_t)s * (kD / 4)];
       o4.x = fmaf(x.x, wt, o4.x); o4.y = fmaf(x.y, wt, o4.y);
       o4.z = fmaf(x.z, wt, o4.z); o4.w = fmaf(x.w, wt, o4.w);
-      L = fmaf(p.ws_l[row0 + s], wt, L);
     }
-  }
-  reinterpret_cast<float4*>(po[w])[lane] = o4;
-  if (lane == 0) { pl[w] = L; if (sub == 0) pm[hd] = M; }
-  __syncthreads();
-  for (int e = tid; e < g * kD; e += 256) {
-    const int hh = e >> 7, c = e & 127;
-    const size_t r = (size_t)b * p.hq + (size_t)h * g + hh;
-    float oo = 0.f, LL = 0.f;
-    for (int s2 = 0; s2 < nsub; ++s2) { oo += po[s2 * g + hh][c]; LL += pl[s2 * g + hh]; }
-    const float Mh = pm[hh];
-    const float wseg = (seg && Mh != -INFINITY) ? exp2f(p.seg_m[r] - Mh) : 0.f;
-    if (seg) LL += p.seg_l[r] * wseg;
-    const float inv = LL > 0.f ? 1.f / LL : 0.f;
-    ot[hh][c] = oo * inv;
-    so[hh][c] = seg ? p.seg_o[r * kD + c] * wseg * inv : 0.f;
-    if (c == 0 && lse) lse[r] = (LL > 0.f) ? (Mh + log2f(LL)) * 0.6931471805599453f : -INFINITY;
+    reinterpret_cast<float4*>(po[w])[lane] = o4;
   }
   __syncthreads();
+  if (tid < kD) {
+    float o = 0.f;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) o += po[i][tid];
+    ot[tid] = o * bc[1];
+  }
+  __syncthreads();
+  const float4 o4 = reinterpret_cast<const float4*>(ot)[lane];
   const float* R = RV + (size_t)h * kD * kD;
-#pragma unroll 2
-  for (int cp = w; cp < kD; cp += 8) {
+  const float sw = bc[2];
+#pragma unroll 4
+  for (int cp = w; cp < kD; cp += 16) {
     const float4 r4 = reinterpret_cast<const float4*>(R + (size_t)cp * kD)[lane];
-    for (int hh = 0; hh < g; ++hh) {
-      const float4 o = reinterpret_cast<const float4*>(ot[hh])[lane];
-      float v = r4.x * o.x + r4.y * o.y + r4.z * o.z + r4.w * o.w;
-      for (int of = 16; of > 0; of >>= 1) v += __shfl_xor_sync(0xffffffffu, v, of);
-      if (lane == hh) {
-        const size_t idx = ((size_t)b * p.hq + (size_t)h * g + hh) * kD + cp;
-        v += so[hh][cp];
-        if (out_fp32) static_cast<float*>(out)[idx] = v;
-        else static_cast<__nv_bfloat16*>(out)[idx] = __float2bfloat16_rn(v);
-      }
+    float v = r4.x * o4.x + r4.y * o4.y + r4.z * o4.z + r4.w * o4.w;
+    for (int of = 16; of > 0; of >>= 1) v += __shfl_xor_sync(0xffffffffu, v, of);
+    if (lane == 0) {
+      if (seg) v += p.seg_o[(size_t)row * kD + cp] * sw;
+      const size_t idx = (size_t)row * kD + cp;
+      if (out_fp32) static_cast<float*>(out)[idx] = v;
+      else static_cast<__nv_bfloat16*>(out)[idx] = __float2bfloat16_rn(v);
     }
   }
 }
@@ -427,7 +450,7 @@ cudaError_t launch_attend(const oscar_ctx& c, const void* q, const int32_t* page
   {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(B, c.hkv);
-    cfg.blockDim = dim3(32 * c.g);
+    cfg.blockDim = dim3(512);
     cfg.dynamicSmemBytes = 0;
     cfg.stream = s;
     cfg.attrs = pdl;
@@ -459,10 +482,10 @@ cudaError_t launch_attend(const oscar_ctx& c, const void* q, const int32_t* page
     if (e != cudaSuccess) return e;
   }
   {
-    const int msmem = 0;
+    const int msmem = p.n_splits * 4;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(B, c.hkv);
-    cfg.blockDim = dim3(256);
+    cfg.gridDim = dim3((unsigned)(B * c.hq));
+    cfg.blockDim = dim3(512);
     cfg.dynamicSmemBytes = msmem;
     cfg.stream = s;
     cfg.attrs = pdl;

@@ -2,7 +2,8 @@
 import csv, io, subprocess, sys
 
 rep = sys.argv[1]
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+kfilt = ["-k", "regex:" + sys.argv[2]] if len(sys.argv) > 2 else []   # optional kernel-name regex
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"] + kfilt, capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 hdr, vals = rows[0], rows[2]
 want = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
@@ -16,7 +17,7 @@ want = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__
 for i, h in enumerate(hdr):
     if any(h == w or (h.startswith(w) and w.endswith("stalled")) for w in want):
         print(f"{h} = {vals[i]} {rows[1][i]}")
-src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"] + kfilt,
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(src)))
 hdr, data = rows[1], rows[2:]

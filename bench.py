@@ -162,6 +162,64 @@ def workload_config(args):
             "l2": "inputs larger than L2: 335.5 MB pool per layer, layers visited in turn"}
 
 
+# ------------------------------------------------------------------ C4 leg
+C4_B, C4_L, C4_HQ, C4_HKV, C4_LAYERS = 16, 131072, 64, 8, 4
+
+
+def c4_leg(args, world, rank, dev, gen, RK_all, RV_all, hbm_peak, peak_kind):
+    """Decode attention at C4 (H_q 64 / H_kv 8, g = 8, 2-bit, G = 64, B = 16, L = 131072): each rank
+    owns 8/N KV heads and their query heads for all sequences (no collective on the path)."""
+    import torch
+    from paper_2605_17757_b200 import binding as Bnd
+    from paper_2605_17757_b200 import synth
+    from paper_2605_17757_b200.parallel import barrier, max_over_ranks
+    hkv = max(1, C4_HKV // world)
+    hq = hkv * (C4_HQ // C4_HKV)
+    o = Bnd.Oscar(Bnd.Config(num_q_heads=hq, num_kv_heads=hkv, bits=BITS, group_size=G, page_size=P))
+    o.set_variant(args.variant)
+    max_pages = C4_L // P
+    pools = [torch.empty((C4_B * max_pages, hkv, o.page_bytes()), dtype=torch.uint8, device=dev)
+             for _ in range(C4_LAYERS)]
+    pt = torch.arange(C4_B * max_pages, dtype=torch.int32, device=dev)
+    pt = pt[torch.randperm(C4_B * max_pages, generator=gen, device=dev)].reshape(C4_B, max_pages).contiguous()
+    RK = [RK_all[l % RK_all.shape[0], :hkv].contiguous() for l in range(C4_LAYERS)]
+    RV = [RV_all[l % RV_all.shape[0], :hkv].contiguous() for l in range(C4_LAYERS)]
+    chunk = 4 * 8192                       # prefill in 32k-token slabs (bounded staging memory)
+    for l in range(C4_LAYERS):
+        for c0 in range(0, C4_B * C4_L, chunk):
+            tok = torch.arange(c0, c0 + chunk, device=dev)
+            b, pos = tok // C4_L, tok % C4_L
+            slots = (pt[b, pos // P].long() * P + pos % P).contiguous()
+            o.quantize_append(synth.torch_keys(gen, chunk, hkv, D, dev), synth.torch_values(gen, chunk, hkv, D, dev),
+                              slots, RK[l], RV[l], pools[l])
+    qs = [synth.torch_decode_q(gen, C4_B, hq, D, dev) for _ in range(C4_LAYERS)]
+    seq = torch.full((C4_B,), C4_L, dtype=torch.int32, device=dev)
+    ws = torch.empty(o.attend_workspace_bytes(C4_B, max_pages), dtype=torch.uint8, device=dev)
+    out = torch.empty((C4_B, hq, D), dtype=torch.bfloat16, device=dev)
+    for _ in range(3):
+        for l in range(C4_LAYERS):
+            o.attend(qs[l], pt, seq, pools[l], RK[l], RV[l], ws, out)
+    torch.cuda.synchronize(); barrier(world)
+    a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = max(5, args.steps)
+    a.record()
+    for _ in range(reps):
+        for l in range(C4_LAYERS):
+            o.attend(qs[l], pt, seq, pools[l], RK[l], RV[l], ws, out)
+    b_.record(); torch.cuda.synchronize()
+    ms = max_over_ranks(a.elapsed_time(b_), world) / (reps * C4_LAYERS)
+    rank_bytes = C4_B * C4_L * hkv * TOKHEAD_BYTES + 2 * C4_B * hq * D * 2
+    del pools
+    return {"config": f"C4: B={C4_B}, L={C4_L}, H_q/H_kv = {C4_HQ}/{C4_HKV} (g=8), b={BITS}, G={G}; "
+                      f"{hkv} kv heads per rank x {world} rank(s); {C4_LAYERS} layer pools in turn",
+            "attend_us": ms * 1e3, "GBps_per_rank": rank_bytes / ms / 1e6,
+            "GBps_aggregate": rank_bytes * world / ms / 1e6,
+            "roofline": {"bound": "hbm", "achieved": rank_bytes / ms / 1e6, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": rank_bytes / ms / 1e6 / hbm_peak, "traffic": None,
+                         "kernel": "oscar_attend (q_rotate+partial+merge), g = 8",
+                         "algorithmic_bytes_per_launch": rank_bytes, "peak_kind": peak_kind}}
+
+
 # ------------------------------------------------------------------ GPU arm
 def main():
     ap = argparse.ArgumentParser()
@@ -172,6 +230,7 @@ def main():
     ap.add_argument("--layers", type=int, default=32)
     ap.add_argument("--variant", type=int, default=0, help="0 = fastest kernels, 1 = simple reference kernels")
     ap.add_argument("--no-extras", action="store_true", help="skip calibration / prefill / e2e / cpu legs (ncu runs)")
+    ap.add_argument("--no-c4", action="store_true", help="skip the C4 (Llama-3-70B-shaped, 128k) decode leg")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -359,6 +418,11 @@ def main():
         e2e = {"value": step_bytes * world * args.steps / (ms_e2e * 1e-3) / 1e9, "unit": "GB/s",
                "h2d_bytes_per_step": NL * (qs[0].numel() + ks[0].numel() + vs[0].numel()) * 2,
                "d2h_bytes_per_step": NL * outs[0].numel() * 2, "ms_per_step": ms_e2e / args.steps}
+
+    # ---------------- C4 leg: Llama-3-70B-shaped GQA decode (g = 8), 128k context; KV heads
+    # partitioned over the ranks, 4 layer pools per rank, attend only
+    if not args.no_extras and not args.no_c4:
+        extras["c4_decode"] = c4_leg(args, world, rank, dev, gen, RK_all, RV_all, hbm_peak, peak_kind)
 
     # ---------------- CPU oracle beside the GPU (rank 0, N=1 only, bounded sample)
     cpu = None

@@ -11,7 +11,8 @@ import os
 from dataclasses import dataclass
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liboscar.so")
+# OSCAR_LIB selects another build of the same library (A/B experiments: tools/ab_attend.sh)
+LIB_PATH = os.environ.get("OSCAR_LIB") or os.path.join(_HERE, "liboscar.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `make` (or __graft_entry__.build()); "

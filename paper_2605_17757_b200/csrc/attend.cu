@@ -379,13 +379,23 @@ __global__ void __launch_bounds__(256) attend_segment_kernel(AttnParams p, const
 // ------------------------------------------------------------------ host side
 // Pages per split (per work item).  Simple kernel: ~8 CTAs per SM over the grid.  Tensor-core
 // kernel: warp-granular items, ~3 per warp of a nominal 16-warps/SM residency, 8..32 pages.
+int attend_mma_total_warps(const oscar_ctx& c);                              // attend_mma.cu
+
+// Pages per split-K work item.  Tensor-core path: as few items as keep every warp of the
+// persistent grid busy — floor(warps / (B·H_kv)) splits per (sequence, kv head) — so each warp
+// gets one balanced item (≤ 32 pages: the partial kernel holds an item's page indices one per
+// lane); fewer, longer items also cut the split partials the merge reads.
 static int choose_pps(const oscar_ctx& c, int B, int max_pages) {
   const long units = (long)B * c.hkv;
-  if (c.pages_per_split > 0)
-    return (c.variant == 0 && attend_mma_supported(c) && c.pages_per_split > 32) ? 32 : c.pages_per_split;
-  if (c.variant == 0 && attend_mma_supported(c)) {
-    long pps = units * max_pages / (3L * c.num_sms * 16);
-    pps = pps < 8 ? 8 : (pps > 32 ? 32 : pps);
+  const bool mma = c.variant == 0 && attend_mma_supported(c);
+  if (c.pages_per_split > 0) return (mma && c.pages_per_split > 32) ? 32 : c.pages_per_split;
+  if (mma) {
+    const long warps = attend_mma_total_warps(c);
+    long splits = units > 0 ? warps / units : 1;
+    if (splits < 1) splits = 1;
+    long pps = (max_pages + splits - 1) / splits;
+    const long lo = max_pages < 4 ? (max_pages > 0 ? max_pages : 1) : 4;
+    pps = pps < lo ? lo : (pps > 32 ? 32 : pps);
     return (int)pps;
   }
   const long target = (long)c.num_sms * 8;
@@ -404,7 +414,6 @@ size_t attend_workspace_bytes(const oscar_ctx& c, int B, int max_pages) {
          (size_t)B * c.hkv * nt * 16 * 32 * 4 + rows * (kD + 2) * 4 + 1024;
 }
 
-int attend_mma_total_warps(const oscar_ctx& c);                              // attend_mma.cu
 cudaError_t launch_attend_mma(const AttnParams& p, int total_warps, cudaStream_t s);
 
 cudaError_t launch_attend(const oscar_ctx& c, const void* q, const int32_t* page_table,

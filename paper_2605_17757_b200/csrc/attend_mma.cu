@@ -13,7 +13,10 @@
 //         per (b, h) by q_rotate_kernel), B = the raw 2/4-bit codes expanded to bytes with one
 //         SHF + LOP3 per 4 codes.  Exact integer dots per (token, head, group); the fp32
 //         epilogue applies s_K, m_K (x̂ = s·c + m).
-//   soft: online softmax in the log2 domain, one max per 64-token chunk, lazy (+8) rescale.
+//   soft: online softmax in the log2 domain, one max per 64-token chunk; the running max
+//         follows every increase (OSCAR_LAZY = 0), so the dominant token's weight is exactly
+//         1 and its PV operand p·s_V is exact in fp16 (a lazy +8 threshold let p reach 2^8 and
+//         put the fp16 rounding of p·s_V on the dominant term: 2.3e-3 max-abs at full size).
 //   PV  : HMMA m16n8k16 f16 -> f32.  A = V codes transposed (channels x tokens): the codes are
 //         masked straight into the fp16 mantissa (subnormal c·2^(b·q)·2^-24, exact), one LOP3
 //         per 2 codes, and each accumulator row is rescaled by 2^(24-b·q) at the end;
@@ -27,6 +30,17 @@ namespace oscar {
 namespace {
 
 constexpr int kWarps = 4;
+#ifndef OSCAR_CHUNK
+#define OSCAR_CHUNK 4
+#endif
+constexpr int kChunk = OSCAR_CHUNK;       // 16-token sub-tiles per softmax chunk
+#ifndef OSCAR_LAZY
+#define OSCAR_LAZY 0
+#endif
+#ifndef OSCAR_MINB
+#define OSCAR_MINB 4
+#endif
+
 
 __device__ __forceinline__ void imma16832(int (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
   asm volatile(
@@ -113,7 +127,7 @@ __device__ __forceinline__ Item decode_item(const AttnParams& p, int it) {
 }  // namespace
 
 template <int BITS, int GQ, int NG>
-__global__ void __launch_bounds__(kWarps * 32, (GQ * NG <= 8 ? 4 : 3))
+__global__ void __launch_bounds__(kWarps * 32, (GQ * NG <= 8 ? OSCAR_MINB : 3))
 attend_partial_mma(AttnParams p, int S) {
   constexpr int NC = GQ * NG;                 // (group, head) combos
   constexpr int NT = (NC + 7) / 8;            // 8-combo tiles (QK M-tiles / PV N-tiles)
@@ -133,6 +147,7 @@ attend_partial_mma(AttnParams p, int S) {
 
   if (lane == 0) {
     for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   }
   __syncwarp();
@@ -146,45 +161,47 @@ attend_partial_mma(AttnParams p, int S) {
   auto fetch_async = [&]() { return lane == 0 ? atomicAdd(p.work, 1) + 2 * total_warps : 0; };
   auto bcast = [&](int v) { return __shfl_sync(0xffffffffu, v, 0); };
   int cur = gw, nxt = gw + total_warps;
-  Item Icur = decode_item(p, cur < n_items ? cur : 0);
-  Item Inxt = decode_item(p, nxt < n_items ? nxt : 0);
-  // page indices of the current / next item: lane l holds page l of the item (pps <= 32)
-  auto load_pages = [&](const Item& L, int it) {
-    return (it < n_items && lane < L.np) ? p.page_table[(size_t)L.b * p.max_pages + L.page0 + lane] : 0;
-  };
-  int pidx_cur = load_pages(Icur, cur), pidx_nxt = load_pages(Inxt, nxt);
-  // load cursor: page lq_k of (lq_sel ? nxt : cur); global page sequence numbers
-  int lq_sel = 0, lq_k = 0;
-  uint32_t seq_issue = 0, seq_use = 0;
-  auto try_issue = [&]() {
-    while ((int)(seq_issue - seq_use) < S) {
-      const bool on_next = lq_sel != 0;
-      if ((on_next ? nxt : cur) >= n_items) break;
-      const Item& L = on_next ? Inxt : Icur;
-      if (lq_k >= L.np) {
-        if (!on_next) { lq_sel = 1; lq_k = 0; continue; }
-        break;
-      }
-      const int64_t page = __shfl_sync(0xffffffffu, on_next ? pidx_nxt : pidx_cur, lq_k);
-      if (lane == 0) {
-        const int s = seq_issue % S;
-        bulk_load(ring + (size_t)s * page_bytes, p.pool + (page * p.hkv + L.h) * (int64_t)page_bytes,
-                  page_bytes, &bars[s], policy);
-      }
-      ++seq_issue;
-      ++lq_k;
+  // loader view of an item: pages, kv head; lane l holds the item's page index l (pps <= 32)
+  int cur_np = 0, cur_h = 0, pidx_cur = 0, nxt_np = 0, nxt_h = 0, pidx_nxt = 0;
+  auto load_item = [&](int it, int& np, int& h, int& pidx) {
+    np = 0; h = 0; pidx = 0;
+    if (it < n_items) {
+      const Item L = decode_item(p, it);
+      np = L.np; h = L.h;
+      if (lane < L.np) pidx = p.page_table[(size_t)L.b * p.max_pages + L.page0 + lane];
     }
   };
+  load_item(cur, cur_np, cur_h, pidx_cur);
+  load_item(nxt, nxt_np, nxt_h, pidx_nxt);
+  // loader: `lq` = stream position of the next page to issue, counted from cur's first page
+  // (pages past cur's end belong to nxt); stages are used in order, one mbarrier each
+  int lq = 0, s_issue = 0, inflight = 0;
+  auto issue_one = [&]() -> bool {
+    const bool in_cur = lq < cur_np;
+    const int kn = lq - cur_np;
+    if (!in_cur && kn >= nxt_np) return false;
+    const int64_t page = __shfl_sync(0xffffffffu, in_cur ? pidx_cur : pidx_nxt, in_cur ? lq : kn);
+    const int h = in_cur ? cur_h : nxt_h;
+    if (lane == 0)
+      bulk_load(ring + (size_t)s_issue * page_bytes, p.pool + (page * p.hkv + h) * (int64_t)page_bytes,
+                page_bytes, &bars[s_issue], policy);
+    s_issue = s_issue + 1 == S ? 0 : s_issue + 1;
+    ++lq;
+    ++inflight;
+    return true;
+  };
   // the first pages depend only on the caller's inputs: start streaming before q_rotate ends
-  try_issue();
+  while (inflight < S && issue_one()) {}
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   int pending = nxt < n_items ? fetch_async() : 0;   // the item after nxt (broadcast when needed)
 
   const int hh = gid % GQ;                    // every tile of this lane serves head hh
   const bool real = NC >= 8 || gid < NC;
+  int s_use = 0;
+  uint32_t ph_use = 0;
 
   while (cur < n_items) {
-    const Item& I = Icur;
+    const Item I = decode_item(p, cur);
     const size_t qrow = (size_t)I.b * p.hq + (size_t)I.h * GQ + hh;
     const float qscale = real ? p.qscale[qrow] : 0.f;
     int grp_of[NT];
@@ -206,18 +223,21 @@ attend_partial_mma(AttnParams p, int S) {
           for (int r = 0; r < 4; ++r) aq[j][kk][r] = qf[(j * 16 + kk * 4 + r) * 32];
     }
     float acc[8][NT][4];
+    float mv_acc[NT];                         // Σ p·m_V of this lane's combo over its tokens
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+    for (int j = 0; j < NT; ++j) {
+      mv_acc[j] = 0.f;
 #pragma unroll
-      for (int j = 0; j < NT; ++j)
+      for (int e = 0; e < 4; ++e)
 #pragma unroll
-        for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.f;
-    float m_run = -INFINITY, l_run = 0.f;
-    float mv_acc[NT];
-#pragma unroll
-    for (int j = 0; j < NT; ++j) mv_acc[j] = 0.f;
+        for (int i = 0; i < 8; ++i) acc[i][j][e] = 0.f;
+    }
+    // scores are kept relative to m_run (log2 domain); m_run starts at 0 and the first chunk
+    // of the item moves it to that chunk's max, later chunks only when the max grows by > 8
+    float m_run = 0.f, l_run = 0.f;
+    bool fresh = true;
 
-    // one page: chunks of up to 4 sub-tiles (64 tokens); FULL = no masking needed
+    // one page: chunks of up to 4 sub-tiles (64 tokens)
     // FULLSUB = 4: a completely valid 64-token page (compile-time shape, no masks);
     // FULLSUB = 0: generic page (any P, masked tail)
     auto page_body = [&](const unsigned char* pg, int valid, auto full_c) {
@@ -226,11 +246,11 @@ attend_partial_mma(AttnParams p, int S) {
       const unsigned char* vcodes = pg + (FULL ? 64 * RB : p.vcodes_off);
       const unsigned char* meta = pg + (FULL ? 128 * RB : p.meta_off);
       const int n_sub = FULL ? FULLSUB : ((valid + 15) >> 4);
-      for (int c0 = 0; c0 < n_sub; c0 += 4) {
-        float sc[4][4];
+      for (int c0 = 0; c0 < n_sub; c0 += kChunk) {
+        float sc[kChunk][4];
         float tmax = -INFINITY;
 #pragma unroll
-        for (int sl = 0; sl < 4; ++sl) {
+        for (int sl = 0; sl < kChunk; ++sl) {
           const int st = c0 + sl;
           if (st >= n_sub) {
 #pragma unroll
@@ -268,7 +288,7 @@ attend_partial_mma(AttnParams p, int S) {
               for (int j = 0; j < NT; ++j) imma16832(cq[j][nt], aq[j][kk], b0, b1);
             }
           }
-          // ---- scores of tokens 4t + e for head hh (log2 domain)
+          // ---- scores of tokens 4t + e for head hh (log2 domain, relative to m_run)
           float part[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
           for (int j = 0; j < NT; ++j) {
@@ -290,40 +310,46 @@ attend_partial_mma(AttnParams p, int S) {
           for (int e = 0; e < 4; ++e) {
             bool ok = real;
             if (!FULL) ok = ok && (16 * st + 4 * t + e) < valid;
-            sc[sl][e] = ok ? part[e] * qscale : -INFINITY;
+            sc[sl][e] = ok ? fmaf(part[e], qscale, -m_run) : -INFINITY;
             tmax = fmaxf(tmax, sc[sl][e]);
           }
         }
         tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 1));
         tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 2));
-        // ---- lazy online-softmax rescale (threshold 2^8)
-        const bool need = tmax > m_run + 8.f;
+        // ---- online-softmax rescale: first chunk of the item, or max grown by > 2^8
+        const bool first = fresh;
+        const bool need = first ? tmax > -INFINITY : tmax > (float)OSCAR_LAZY;
+        fresh = false;
         if (__any_sync(0xffffffffu, need)) {
-          const float m_new = need ? tmax : m_run;
-          const float alpha = need ? exp2f(m_run - m_new) : 1.f;
-          l_run *= alpha;
+          const float shift = need ? tmax : 0.f;
+          const float alpha = first ? 1.f : ex2_ftz(-shift);   // nothing accumulated yet if first
 #pragma unroll
-          for (int j = 0; j < NT; ++j) mv_acc[j] *= alpha;
-          m_run = m_new;
+          for (int sl = 0; sl < kChunk; ++sl)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) sc[sl][e] -= shift;
+          m_run += shift;
+          l_run *= alpha;
           const float a0 = __shfl_sync(0xffffffffu, alpha, 8 * t);
           const float a1 = __shfl_sync(0xffffffffu, alpha, 8 * t + 4);
 #pragma unroll
-          for (int i = 0; i < 8; ++i)
+          for (int j = 0; j < NT; ++j) {
+            mv_acc[j] *= alpha;
 #pragma unroll
-            for (int j = 0; j < NT; ++j) {
+            for (int i = 0; i < 8; ++i) {
               acc[i][j][0] *= a0; acc[i][j][2] *= a0;
               acc[i][j][1] *= a1; acc[i][j][3] *= a1;
             }
+          }
         }
         // ---- PV per sub-tile
 #pragma unroll
-        for (int sl = 0; sl < 4; ++sl) {
+        for (int sl = 0; sl < kChunk; ++sl) {
           const int st = c0 + sl;
           if (st >= n_sub) break;
           float pr[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            pr[e] = ex2_ftz(sc[sl][e] - m_run);    // exp2(-inf) = 0 (m_run finite here)
+            pr[e] = ex2_ftz(sc[sl][e]);            // exp2(-inf) = 0
             l_run += pr[e];
           }
           uint32_t bpv[NT][2];
@@ -334,6 +360,7 @@ attend_partial_mma(AttnParams p, int S) {
             float w4[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
+              // p·s_V and p·m_V in fp32 (one fp16 rounding of the MMA operand; the m_V sum exact)
               const __half2 smv = *reinterpret_cast<const __half2*>(&mw[e]);
               if (FULL) {
                 w4[e] = pr[e] * __low2float(smv);
@@ -374,19 +401,17 @@ attend_partial_mma(AttnParams p, int S) {
       }
     };
 
-    try_issue();
     for (int k = 0; k < I.np; ++k) {
-      const int s = seq_use % S;
-      mbar_wait(&bars[s], (seq_use / S) & 1);
-      const unsigned char* pg = ring + (size_t)s * page_bytes;
+      mbar_wait(&bars[s_use], ph_use);
+      const unsigned char* pg = ring + (size_t)s_use * page_bytes;
       const int valid = min(P, I.seq_len - (I.page0 + k) * P);
       if (valid == 64 && P == 64) page_body(pg, valid, std::integral_constant<int, 4>{});
       else page_body(pg, valid, std::integral_constant<int, 0>{});
-      // release the stage, keep the ring full (possibly with the next item's pages)
+      // release the stage (every lane's reads are done) and refill it
       __syncwarp();
-      ++seq_use;
-      if (lane == 0) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      try_issue();
+      if (++s_use == S) { s_use = 0; ph_use ^= 1u; }
+      --inflight;
+      issue_one();
     }
 
     // ---- write this item's partial (unnormalized õ in the rotated frame, m, l)
@@ -399,36 +424,35 @@ attend_partial_mma(AttnParams p, int S) {
     }
     const size_t row0 = ((size_t)I.b * p.hq + (size_t)I.h * GQ) * p.n_splits + I.split;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const float unscale = (float)(1 << (24 - BITS * (i % CPB)));
+    for (int j = 0; j < NT; ++j)
 #pragma unroll
-      for (int j = 0; j < NT; ++j)
+      for (int e = 0; e < 4; ++e) {
+        const int col = 2 * t + (e & 1);
+        const int cc = 8 * j + col;
+        const float mvs = __shfl_sync(0xffffffffu, mv_acc[j], 4 * col);   // combo col = gid of lane 4·col
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int col = 2 * t + (e & 1);
-          const int cc = 8 * j + col;
+        for (int i = 0; i < 8; ++i) {
+          const float unscale = (float)(1 << (24 - BITS * (i % CPB)));
           const int ch = pv_channel<BITS>(i, gid, e >> 1);
-          const float mvs = __shfl_sync(0xffffffffu, mv_acc[j], 4 * col);
           if (cc < NC && ch / G == cc / GQ) {
             const size_t row = row0 + (size_t)(cc % GQ) * p.n_splits;
             p.ws_o[row * 128 + ch] = fmaf(acc[i][j][e], unscale, mvs);
           }
         }
-    }
+      }
     if (t == 0 && gid < GQ) {
       const size_t row = row0 + (size_t)gid * p.n_splits;
-      p.ws_m[row] = m_run;
+      p.ws_m[row] = I.np > 0 ? m_run : -INFINITY;
       p.ws_l[row] = l_run;
     }
     // ---- advance: the loader already moved on to `nxt`
+    lq -= cur_np;
     cur = nxt;
-    Icur = Inxt;
-    pidx_cur = pidx_nxt;
-    if (lq_sel) lq_sel = 0; else lq_k = 0;
+    cur_np = nxt_np; cur_h = nxt_h; pidx_cur = pidx_nxt;
     nxt = cur < n_items ? bcast(pending) : n_items;
-    if (nxt < n_items) Inxt = decode_item(p, nxt);
-    pidx_nxt = load_pages(Inxt, nxt);
+    load_item(nxt, nxt_np, nxt_h, pidx_nxt);
     pending = nxt < n_items ? fetch_async() : 0;
+    while (inflight < S && issue_one()) {}
   }
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");   // let the merge kernel launch
 }
@@ -470,13 +494,20 @@ int attend_mma_total_warps(const oscar_ctx& c) {
   if (!fn) return 0;
   const int S = stages_for(c.page_bytes);
   const int smem = kWarps * S * (c.page_bytes + 8);
+  // resident CTAs per SM, cached per (kernel, smem): the query is a few µs of host time
+  static struct { KernelFn fn; int smem, per_sm; } cache[16];
+  for (auto& e : cache)
+    if (e.fn == fn && e.smem == smem) return c.num_sms * e.per_sm * kWarps;
   int per_sm = 0;
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess ||
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kWarps * 32, smem) != cudaSuccess) {
     cudaGetLastError();
     per_sm = 2;
   }
-  return c.num_sms * (per_sm > 0 ? per_sm : 1) * kWarps;
+  if (per_sm < 1) per_sm = 1;
+  for (auto& e : cache)
+    if (e.fn == nullptr) { e.fn = fn; e.smem = smem; e.per_sm = per_sm; break; }
+  return c.num_sms * per_sm * kWarps;
 }
 
 cudaError_t launch_attend_mma(const AttnParams& p, int total_warps, cudaStream_t s) {

@@ -162,6 +162,8 @@ def _run_attend(o, q, pt, L, pool, RK, RV):
     dict(name="C2small", Hq=32, Hkv=8, bits=2, G=64, B=3, L=[1000, 77, 0]),
     dict(name="g8", Hq=16, Hkv=2, bits=2, G=128, B=2, L=[513, 64]),
     dict(name="g2b4", Hq=4, Hkv=2, bits=4, G=64, B=2, L=[300, 1]),
+    dict(name="C4small", Hq=16, Hkv=2, bits=2, G=64, B=2, L=[700, 130]),     # g=8, two 8-combo tiles
+    dict(name="g4G32", Hq=8, Hkv=2, bits=4, G=32, B=2, L=[450, 64]),        # 4 groups x 4 heads
 ])
 @pytest.mark.parametrize("variant", [0, 1])
 @pytest.mark.parametrize("pps", [0, 1, 3])

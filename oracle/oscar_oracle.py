@@ -210,7 +210,10 @@ def quantize_rows(Xc: np.ndarray, bits: int, G: int):
     s32 = s16.astype(np.float32)
     inv = np.where(s32 > 0, np.float32(1.0) / np.where(s32 > 0, s32, np.float32(1.0)), np.float32(0.0))
     inv = inv.astype(np.float32)
-    t = (Xg - m16.astype(np.float32)[..., None]) * inv[..., None]   # two fp32 roundings
+    dx = Xg - m16.astype(np.float32)[..., None]                      # fp32 RN
+    # reading Z4: the product dx·inv is taken exactly (fp32 x fp32 fits fp64's 53 bits) and
+    # rounded once, to the nearest integer (half-even) -- P:L1286-1295's real-arithmetic round
+    t = dx.astype(np.float64) * inv.astype(np.float64)[..., None]
     c = np.clip(np.rint(t), 0, qmax).astype(np.uint8)               # np.rint = half-even
     return c.reshape(Xc.shape), s16, m16
 

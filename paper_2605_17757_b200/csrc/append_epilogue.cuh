@@ -32,9 +32,12 @@ __device__ __forceinline__ void minmax_params(float mn, float mx, float qmax, __
   inv = sf > 0.f ? __fdiv_rn(1.f, sf) : 0.f;
 }
 
+// reading Z4: c = clamp(rint(RN(x - m)·inv), 0, qmax) with the product exact: one FFMA with the
+// 1.5·2^23 magic constant rounds the exact product to an integer (half-even); the clamp acts on
+// the float bits (any |product| >= 2^22 lands outside [magic, magic + qmax] on the right side)
 __device__ __forceinline__ int quant_code(float x, float m, float inv, int qmax) {
-  const float t = __fmul_rn(__fsub_rn(x, m), inv);
-  return min(max(__float2int_rn(t), 0), qmax);
+  const float tq = __fmaf_rn(__fsub_rn(x, m), inv, 12582912.f);
+  return min(max(__float_as_int(tq), 0x4B400000), 0x4B400000 + qmax) - 0x4B400000;
 }
 
 // Nearest-rank clip threshold over a 128-value row held 4 per lane (reading Z6):

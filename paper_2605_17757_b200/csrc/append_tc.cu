@@ -1,20 +1,24 @@
 // Tensor-core quantize_append (variant 0).  Alg. 1 `Prefill` rotate-before-
 // write + `QuantizeAndWrite`; §4 "KV Cache Update".
 //
-// Persistent CTA per (kv head, K|V) "pair" slice, 10 warps:
+// Persistent CTA per (kv head, K|V) "pair" slice, 18 warps:
 //   warp 0      TMA producer: 128-token x 128-channel bf16 tiles of K (or V) for one head,
-//               two 64-channel SWIZZLE_128B boxes per tile, 3-stage smem ring
+//               two 64-channel SWIZZLE_128B boxes per tile, 4-stage smem ring
 //   warp 1      TMEM allocator (256 columns = 2 fp32 accumulators) + single-thread tcgen05.mma
 //               issuer: x̃ = [x x]·[R_hi; R_lo] as 16 UMMA 128x128x16 (bf16 -> fp32 TMEM).  The
 //               bf16 hi/lo split of the fp32 R keeps rotated values within 1e-5 of the fp64
 //               product; R_hi, R_lo stay resident in smem (K-major SW128).
-//   warps 2-9   epilogue: tcgen05.ld 32x32b (thread = token row, 64 channels each), per-group
-//               min/max, fp16 (s, m), codes with the reading-Z4 fp32 operation order, pack, and
-//               store into the slot's page block (FORMAT, common.cuh).
+//   warps 2-17  epilogue, 4 per TMEM lane quarter = (channel half) x (tile parity): tcgen05.ld
+//               32x32b (thread = token row, 64 channels), per-group min/max, fp16 (s, m), codes
+//               (reading Z4: one FFMA + bit clamp per code), pack, store into the slot's page
+//               block (FORMAT, common.cuh); V codes of whole 16-token tiles are staged in smem in
+//               FORMAT order and written as 16-B chunks.
 // Scope of this kernel: b in {2, 4}, G in {32, 64}, no clipping; other configs use the simple
 // kernel (append.cu).
 #include <cuda.h>
 #include <cudaTypedefs.h>
+
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -23,16 +27,19 @@ namespace oscar {
 namespace {
 
 constexpr int kTok = 128;          // tokens per tile (UMMA M)
-constexpr int kStages = 3;
-constexpr int kEpiWarps = 8;
+constexpr int kStages = 4;
+constexpr int kEpiWarps = 16;                   // 4 per TMEM lane quarter: (channel half, tile parity)
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr int kTileBytes = kTok * kD * 2;       // 32 KB bf16 tile
 constexpr int kBBytes = kD * kD * 2;            // 32 KB bf16 R part
+
+constexpr int kVStage = 2 * (16 * 64 + 16);    // V codes of one 32-token quarter (b <= 4), 2 padded tiles
 
 struct TcSmem {
   alignas(1024) uint8_t Bhi[kBBytes];           // [2 k-chunks][128 rows n][128 B], SW128
   alignas(1024) uint8_t Blo[kBBytes];
   alignas(1024) uint8_t A[kStages][kTileBytes]; // [stage][2 k-chunks][128 rows tok][128 B]
+  alignas(16) uint8_t vstage[2][4][kVStage];    // per (tile parity, lane quarter): FORMAT-ordered V codes
   uint64_t full[kStages], empty[kStages], tfull[2], tempty[2];
   uint32_t tmem_base;
 };
@@ -103,6 +110,15 @@ struct TcParams {
   int cpp, tiles_per_pair;
 };
 
+// Σ_i 0x4B400000 << (BITS·i) mod 2^32 over the codes of one 32-bit word: the constant part of
+// the accumulated magic-add float bits
+template <int BITS>
+__device__ __forceinline__ constexpr uint32_t magic_words() {
+  uint32_t k = 0;
+  for (int i = 0; i < 32 / BITS; ++i) k += 0x4B400000u << (BITS * i);
+  return k;
+}
+
 }  // namespace
 
 template <int BITS, int G>
@@ -141,7 +157,7 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
   }
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) { mbar_init(&S.full[s], 1); mbar_init(&S.empty[s], 1); }
-    for (int a = 0; a < 2; ++a) { mbar_init(&S.tfull[a], 1); mbar_init(&S.tempty[a], kEpiWarps); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&S.tfull[a], 1); mbar_init(&S.tempty[a], kEpiWarps / 2); }
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;\n" ::"r"(su32(&S.tmem_base)));
@@ -194,15 +210,26 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
       __syncwarp();
     }
   } else {
-    // ================= epilogue: thread = token row, 64 channels (half of the row)
+    // ================= epilogue: thread = token row, 64 channels (half of the row); the warps
+    // of a lane quarter split by (channel half, tile parity), so the two TMEM accumulators are
+    // drained concurrently
     const int ew = warp - 2;
     const int quarter = warp & 3;                 // TMEM lane quarter this warp may access
-    const int half = ew >> 2;                     // channels [64·half, 64·half + 64)
+    const int half = (ew >> 2) & 1;               // channels [64·half, 64·half + 64)
+    const int par = ew >> 3;                      // tiles i with i % 2 == par (accumulator par)
     const int r = quarter * 32 + lane;            // row (token) within the tile
     constexpr int QMAX = (1 << BITS) - 1;
     constexpr int GPH = 64 / G;                   // groups in this half
-    for (int i = 0; i < ntiles; ++i) {
-      const int a = i & 1;
+    // slot of this thread's token, loaded one tile ahead (its latency is off the critical path)
+    auto load_slot = [&](int i) -> int64_t {
+      const int64_t tk = (int64_t)(sub + i * p.cpp) * kTok + r;
+      return (i < ntiles && tk < p.T) ? p.slots[tk] : -1;
+    };
+    int64_t slot_next = load_slot(par);
+    for (int i = par; i < ntiles; i += 2) {
+      const int a = par;
+      const int64_t slot = slot_next;
+      slot_next = load_slot(i + 2);
       mbar_wait(&S.tfull[a], (i >> 1) & 1);
       fence_after();
       uint32_t v[64];
@@ -214,15 +241,22 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.tempty[a]);
 
-      const int64_t tok = (int64_t)(sub + i * p.cpp) * kTok + r;
-      if (tok >= p.T) continue;
-      const int64_t slot = p.slots[tok];
+      const bool valid = slot >= 0;
+      // V fast path: the quarter's 32 tokens go to 32 consecutive slots starting on a 16-token
+      // tile, i.e. two whole 16-token FORMAT tiles -> stage the FORMAT-ordered bytes in smem and
+      // write 16-B chunks.  Both warps of the quarter (the two channel halves) see the same rows,
+      // so they take the same branch and meet at the same named barrier.
+      const int64_t slot0 = __shfl_sync(0xffffffffu, slot, 0);
+      const bool fastV = isV && __all_sync(0xffffffffu, valid && slot == slot0 + lane && (slot0 & 15) == 0);
+      if (!valid) continue;
       const int64_t page = slot / p.P;
       const int u = (int)(slot % p.P);
       uint8_t* blk = p.pool + (page * p.hkv + h) * (int64_t)p.page_bytes;
-      uint32_t packed[BITS * 2];                  // 64 codes · BITS bits = BITS·2 words
+      // codes: the magic add leaves float bits 0x4B400000 + code; accumulate bits << shift with
+      // one LEA per code and remove the constant part once per word
+      uint32_t packed[BITS * 2];
 #pragma unroll
-      for (int w = 0; w < BITS * 2; ++w) packed[w] = 0;
+      for (int w = 0; w < BITS * 2; ++w) packed[w] = 0u - magic_words<BITS>();
 #pragma unroll
       for (int gi = 0; gi < GPH; ++gi) {
         float mn = __uint_as_float(v[gi * G]), mx = mn;
@@ -238,24 +272,57 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
         const float inv = sf > 0.f ? __fdiv_rn(1.f, sf) : 0.f;
 #pragma unroll
         for (int c = 0; c < G; ++c) {
-          // t = (x - m)·inv (RN, RN), rint via the 1.5·2^23 magic add (round-half-even),
-          // clamp on the float bits (same exponent), low bits = code
-          const float tq = __fadd_rn(__fmul_rn(__fsub_rn(__uint_as_float(v[gi * G + c]), m), inv), 12582912.f);
-          const int bits = min(max(__float_as_int(tq), 0x4B400000), 0x4B400000 + QMAX);
+          // reading Z4: rint(RN(x - m)·inv) with the exact product: one FFMA with the 1.5·2^23
+          // magic constant (round-half-even), clamp on the float bits (same exponent)
+          const float tq = __fmaf_rn(__fsub_rn(__uint_as_float(v[gi * G + c]), m), inv, 12582912.f);
+          const uint32_t bits = (uint32_t)min(max(__float_as_int(tq), 0x4B400000), 0x4B400000 + QMAX);
           const int idx = gi * G + c;             // code index within the half row
-          packed[idx * BITS / 32] |= (uint32_t)(bits & QMAX) << ((idx * BITS) & 31);
+          packed[idx * BITS / 32] += bits << ((idx * BITS) & 31);
         }
         const int grp = (half * 64 + gi * G) / G;
         *reinterpret_cast<__half2*>(blk + p.meta_off + fmt_meta(u, grp, p.ng) + (isV ? 16 : 0)) =
             __halves2half2(s16, m16);
       }
       constexpr int HB = 8 * BITS;                // bytes of this half row
+      constexpr int RB = 16 * BITS;               // bytes of a row
       if (!isV) {
         uint8_t* dst = blk + fmt_krow(u) * p.row_bytes + half * HB;
 #pragma unroll
         for (int w4 = 0; w4 < BITS / 2; ++w4)
           *reinterpret_cast<uint4*>(dst + 16 * w4) =
               make_uint4(packed[4 * w4], packed[4 * w4 + 1], packed[4 * w4 + 2], packed[4 * w4 + 3]);
+      } else if (fastV) {
+        constexpr int TILE = 16 * RB + 16;        // staged 16-token tile (+16 B: bank shift)
+        const uint32_t stg = su32(S.vstage[par][quarter]);
+        // this token's bytes at their FORMAT offsets inside its 16-token tile (fmt_vbyte with
+        // u = lane % 16: compile-time part per byte + 16·(4-token group) + token-in-group)
+        const uint32_t base = stg + (lane >> 4) * TILE + 16 * ((lane >> 2) & 3) + (lane & 3);
+        auto put = [&](auto half_c) {
+          constexpr int H = decltype(half_c)::value;
+#pragma unroll
+          for (int jb = 0; jb < HB; ++jb)
+            asm volatile("st.shared.u8 [%0], %1;\n" ::"r"(base + fmt_vbyte(0, H * HB + jb, RB)),
+                         "r"(packed[jb >> 2] >> (8 * (jb & 3))) : "memory");
+        };
+        if (half) put(std::integral_constant<int, 1>{});
+        else put(std::integral_constant<int, 0>{});
+        const int bar_id = 1 + quarter + 4 * par;
+        asm volatile("bar.sync %0, 64;\n" ::"r"(bar_id) : "memory");
+        // copy out: 2 tiles x 16·RB bytes, 16 B per thread per pass (64 threads)
+        const int tp = half * 32 + lane;
+#pragma unroll
+        for (int pass = 0; pass < (2 * 16 * RB) / (16 * 64); ++pass) {
+          const int cidx = pass * 64 + tp;        // 16-B chunk within the quarter
+          const int tile = cidx / RB;             // RB chunks of 16 B per 16-token tile
+          const int64_t sl = slot0 + 16 * tile;
+          uint8_t* dst = p.pool + ((sl / p.P) * p.hkv + h) * (int64_t)p.page_bytes + p.vcodes_off +
+                         16 * RB * (int)((sl % p.P) >> 4) + 16 * (cidx % RB);
+          uint4 q;
+          asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n"
+                       : "=r"(q.x), "=r"(q.y), "=r"(q.z), "=r"(q.w) : "r"(stg + tile * TILE + 16 * (cidx % RB)));
+          *reinterpret_cast<uint4*>(dst) = q;
+        }
+        asm volatile("bar.sync %0, 64;\n" ::"r"(bar_id) : "memory");   // staging reusable
       } else {
         uint8_t* vb = blk + p.vcodes_off;
 #pragma unroll

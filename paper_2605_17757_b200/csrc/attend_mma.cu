@@ -30,6 +30,9 @@ namespace oscar {
 namespace {
 
 constexpr int kWarps = 4;
+#ifndef OSCAR_QK_LSHIFT
+#define OSCAR_QK_LSHIFT 0
+#endif
 #ifndef OSCAR_CHUNK
 #define OSCAR_CHUNK 4
 #endif
@@ -203,14 +206,20 @@ attend_partial_mma(AttnParams p, int S) {
   while (cur < n_items) {
     const Item I = decode_item(p, cur);
     const size_t qrow = (size_t)I.b * p.hq + (size_t)I.h * GQ + hh;
+#if OSCAR_QK_LSHIFT
+    constexpr float kBScale = (float)(1 << (8 - BITS));   // B bytes carry c·2^(8-BITS)
+    const float qscale = real ? p.qscale[qrow] * (1.f / kBScale) : 0.f;
+#else
+    constexpr float kBScale = 1.f;
     const float qscale = real ? p.qscale[qrow] : 0.f;
+#endif
     int grp_of[NT];
     float qsumf[NT];
 #pragma unroll
     for (int j = 0; j < NT; ++j) {
       const int c = 8 * j + gid;
       grp_of[j] = c < NC ? c / GQ : 0;
-      qsumf[j] = c < NC ? (float)p.qsum[qrow * 8 + grp_of[j]] : 0.f;
+      qsumf[j] = c < NC ? (float)p.qsum[qrow * 8 + grp_of[j]] * kBScale : 0.f;
     }
     uint32_t aq[NT][4][4];
     {
@@ -277,6 +286,18 @@ attend_partial_mma(AttnParams p, int S) {
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {
               uint32_t b0, b1;
+#if OSCAR_QK_LSHIFT
+              // codes moved to the top bits of each byte with a left shift (a multiply: FMA
+              // pipe) and one mask: every B byte is c·2^(8-BITS), folded into qscale
+              constexpr uint32_t kTopMask = kByteMask << (8 - BITS);
+              if (BITS == 2) {
+                b0 = (w[0] * (1u << (6 - 2 * kk))) & kTopMask;
+                b1 = (w[1] * (1u << (6 - 2 * kk))) & kTopMask;
+              } else {
+                b0 = (w[kk >> 1] * (1u << (4 - 4 * (kk & 1)))) & kTopMask;
+                b1 = (w[2 + (kk >> 1)] * (1u << (4 - 4 * (kk & 1)))) & kTopMask;
+              }
+#else
               if (BITS == 2) {
                 b0 = (w[0] >> (2 * kk)) & kByteMask;
                 b1 = (w[1] >> (2 * kk)) & kByteMask;
@@ -284,6 +305,7 @@ attend_partial_mma(AttnParams p, int S) {
                 b0 = (w[kk >> 1] >> (4 * (kk & 1))) & kByteMask;
                 b1 = (w[2 + (kk >> 1)] >> (4 * (kk & 1))) & kByteMask;
               }
+#endif
 #pragma unroll
               for (int j = 0; j < NT; ++j) imma16832(cq[j][nt], aq[j][kk], b0, b1);
             }

@@ -93,11 +93,27 @@ def _decode_pool(pool, slots, H, fmt):
     return out
 
 
-@pytest.mark.parametrize("bits,G,rho,variant,Tn", [(2, 64, (1.0, 1.0), 0, 1000), (4, 32, (0.96, 0.92), 0, 1000),
-                                                   (2, 64, (1.0, 1.0), 1, 1000), (2, 32, (1.0, 1.0), 0, 16),
-                                                   (4, 64, (1.0, 1.0), 0, 300), (4, 32, (1.0, 1.0), 0, 1280),
-                                                   (2, 128, (1.0, 1.0), 0, 129)])
-def test_quantize_append_parity(bits, G, rho, variant, Tn):
+def _slots(rng, mode, Tn, npages):
+    """perm: random distinct slots.  contigN: the first 700 tokens take consecutive slots from
+    slot N (a 16-aligned N exercises the tensor-core kernel's staged V path, also across page
+    boundaries), the rest random distinct slots."""
+    if mode == "perm":
+        return rng.permutation(npages * 64)[:Tn].astype(np.int64)
+    start = int(mode[6:])
+    run = np.arange(start, start + 700)
+    rest = np.setdiff1d(np.arange(npages * 64), run)
+    return np.concatenate([run, rng.permutation(rest)[:Tn - 700]]).astype(np.int64)
+
+
+@pytest.mark.parametrize("bits,G,rho,variant,Tn,slot_mode", [
+    (2, 64, (1.0, 1.0), 0, 1000, "perm"), (4, 32, (0.96, 0.92), 0, 1000, "perm"),
+    (2, 64, (1.0, 1.0), 1, 1000, "perm"), (2, 32, (1.0, 1.0), 0, 16, "perm"),
+    (4, 64, (1.0, 1.0), 0, 300, "perm"), (4, 32, (1.0, 1.0), 0, 1280, "perm"),
+    (2, 128, (1.0, 1.0), 0, 129, "perm"),
+    (2, 64, (1.0, 1.0), 0, 1000, "contig208"), (4, 64, (1.0, 1.0), 0, 1000, "contig208"),
+    (2, 32, (1.0, 1.0), 0, 1000, "contig200"), (4, 32, (1.0, 1.0), 0, 1280, "contig0"),
+])
+def test_quantize_append_parity(bits, G, rho, variant, Tn, slot_mode):
     torch = _torch()
     rng = np.random.default_rng(7 + bits + G + Tn)
     H, npages = 8, 21
@@ -105,7 +121,7 @@ def test_quantize_append_parity(bits, G, rho, variant, Tn):
     K = synth.gen_keys(rng, Tn, H, 128)
     V = synth.gen_values(rng, Tn, H, 128)
     RK, RV = synth.gen_rotation(rng, H, 128), synth.gen_rotation(rng, H, 128)
-    slots = rng.permutation(npages * 64)[:Tn].astype(np.int64)
+    slots = _slots(rng, slot_mode, Tn, npages)
     ref = np.zeros((npages, H, fmt.page_bytes), np.uint8)
     O.quantize_append(K, V, slots, RK, RV, fmt, ref, rho[0], rho[1])
     o = make(num_q_heads=H * 4, num_kv_heads=H, bits=bits, group_size=G, clip_ratio_k=rho[0],

@@ -63,7 +63,8 @@ typedef struct {
   int32_t head_dim;        /* d; must be a power of two; this build implements d = 128       */
   int32_t num_q_heads;     /* H_q of this rank's shard                                       */
   int32_t num_kv_heads;    /* H_kv of this shard; H_q % H_kv == 0, g = H_q / H_kv (GQA)       */
-  int32_t bits;            /* b in {2, 4} (3 is accepted by the oracle only: UNSUPPORTED here)*/
+  int32_t bits;            /* b in {2, 3, 4}; b = 3 (codes straddle bytes, reading Z23) runs on
+                              the simple CUDA-core kernels, b = 2, 4 also on the tensor-core ones */
   int32_t group_size;      /* G in {32, 64, 128}, G | d; same for K and V (reading Z7)        */
   int32_t page_size;       /* P tokens per page; multiple of 16; 0 => 64                       */
   float clip_ratio_k;      /* rho_K in (0, 1]; 1 = no clipping (App A.5)         */
@@ -112,7 +113,9 @@ OSCAR_API oscar_status oscar_calib_finalize(const oscar_ctx* ctx, const double* 
  * codes with fp16 (s, m) metadata (reading Z4 operation order), bit-pack, and store into
  * the slot's page block (FORMAT above).
  * K, V: bf16 [T][H_kv][d]; slots: int64 [T] (page·P + offset); R_K, R_V: fp32 [H_kv][d][d];
- * pool: see oscar_page_bytes.  T = 0 is a no-op. */
+ * pool: see oscar_page_bytes.  T = 0 is a no-op.
+ * R_V = NULL selects the pre-rotated-V mode ("absorb R_V into W_V"):
+ * V rows are taken as already rotated (identity rotation); pass NULL to oscar_attend too. */
 OSCAR_API oscar_status oscar_quantize_append(const oscar_ctx* ctx, const void* K, const void* V,
                                    const int64_t* slots, int64_t T, const float* R_K,
                                    const float* R_V, void* pool, void* stream);
@@ -125,7 +128,8 @@ OSCAR_API oscar_status oscar_quantize_append(const oscar_ctx* ctx, const void* K
  * q: bf16 [B][H_q][d]; page_table: int32 [B][max_pages]; seq_lens: int32 [B] (<= max_pages·P,
  * 0 => o = 0, lse = -inf); pool as written by oscar_quantize_append; workspace: device bytes
  * >= oscar_attend_workspace_bytes(ctx, B, max_pages); out: [B][H_q][d] bf16 (out_fp32 = 0)
- * or fp32 (out_fp32 = 1); lse: fp32 [B][H_q] natural-log sum-exp of ℓ, or NULL. */
+ * or fp32 (out_fp32 = 1); lse: fp32 [B][H_q] natural-log sum-exp of ℓ, or NULL.
+ * R_V = NULL (pre-rotated-V mode, NEXT-2): o = õ, returned in V's own (rotated) frame. */
 OSCAR_API size_t oscar_attend_workspace_bytes(const oscar_ctx* ctx, int32_t B, int32_t max_pages);
 OSCAR_API oscar_status oscar_attend(const oscar_ctx* ctx, const void* q, const int32_t* page_table,
                           const int32_t* seq_lens, int32_t B, int32_t max_pages,

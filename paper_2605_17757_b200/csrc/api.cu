@@ -66,7 +66,6 @@ oscar_status oscar_create(const oscar_config* cfg, oscar_ctx** out) {
   if (g > 8) return fail(OSCAR_ERR_UNSUPPORTED, "GQA ratio %d > 8 not implemented", g);
   if (c.bits != 2 && c.bits != 3 && c.bits != 4)
     return fail(OSCAR_ERR_ARG, "bits must be 2, 3 or 4 (got %d)", c.bits);
-  if (c.bits == 3) return fail(OSCAR_ERR_UNSUPPORTED, "3-bit codes are not implemented on the GPU path");
   if (c.group_size != 32 && c.group_size != 64 && c.group_size != 128)
     return fail(OSCAR_ERR_ARG, "group_size must be 32, 64 or 128 (got %d)", c.group_size);
   const int P = c.page_size == 0 ? 64 : c.page_size;
@@ -158,7 +157,7 @@ oscar_status oscar_quantize_append(const oscar_ctx* ctx, const void* K, const vo
   if (!ctx) return fail(OSCAR_ERR_ARG, "NULL ctx");
   if (T < 0) return fail(OSCAR_ERR_ARG, "T must be >= 0");
   if (T == 0) return OSCAR_OK;
-  if (!K || !V || !slots || !R_K || !R_V || !pool) return fail(OSCAR_ERR_ARG, "oscar_quantize_append: NULL pointer");
+  if (!K || !V || !slots || !R_K || !pool) return fail(OSCAR_ERR_ARG, "oscar_quantize_append: NULL pointer");
   cudaStream_t s = as_stream(stream);
   if (ctx->variant == 0 && oscar::append_small_ok(*ctx, T))      // decode-size: latency path
     return cuda_status(oscar::launch_append_small(*ctx, K, V, slots, T, R_K, R_V, pool, s), "append_small");
@@ -204,7 +203,7 @@ oscar_status oscar_attend(const oscar_ctx* ctx, const void* q, const int32_t* pa
   if (B < 0 || max_pages < 0) return fail(OSCAR_ERR_ARG, "B and max_pages must be >= 0");
   if (B == 0) return OSCAR_OK;
   if (max_pages == 0) return fail(OSCAR_ERR_ARG, "max_pages must be > 0");
-  if (!q || !page_table || !seq_lens || !pool || !R_K || !R_V || !workspace || !out)
+  if (!q || !page_table || !seq_lens || !pool || !R_K || !workspace || !out)
     return fail(OSCAR_ERR_ARG, "oscar_attend: NULL pointer");
   const size_t need = oscar::attend_workspace_bytes(*ctx, B, max_pages);
   if (workspace_bytes < need)
@@ -227,7 +226,7 @@ oscar_status oscar_attend_mixed(const oscar_ctx* ctx, const void* q, const int32
   if (max_pages == 0) return fail(OSCAR_ERR_ARG, "max_pages must be > 0");
   if (seg_cap == 0 || seg_cap > 1024)
     return fail(OSCAR_ERR_ARG, "seg_cap must be in [1, 1024] (got %d)", seg_cap);
-  if (!q || !page_table || !seq_lens || !pool || !R_K || !R_V || !workspace || !out || !seg_k || !seg_v ||
+  if (!q || !page_table || !seq_lens || !pool || !R_K || !workspace || !out || !seg_k || !seg_v ||
       !seg_lens)
     return fail(OSCAR_ERR_ARG, "oscar_attend_mixed: NULL pointer");
   const size_t need = oscar::attend_workspace_bytes(*ctx, B, max_pages);

@@ -29,9 +29,14 @@ __global__ void __launch_bounds__(128) append_simple_kernel(
   const int tid = threadIdx.x;
 
   if (mode != 2) {
-    const float* R = (isV ? RV : RK) + (size_t)h * kD * kD;
-    for (int e = tid; e < kD * kD / 4; e += 128)
-      reinterpret_cast<float4*>(Rs)[e] = reinterpret_cast<const float4*>(R)[e];
+    const float* Rb = isV ? RV : RK;      // R_V = NULL: pre-rotated V (NEXT-2) -> identity
+    if (Rb) {
+      const float* R = Rb + (size_t)h * kD * kD;
+      for (int e = tid; e < kD * kD / 4; e += 128)
+        reinterpret_cast<float4*>(Rs)[e] = reinterpret_cast<const float4*>(R)[e];
+    } else {
+      for (int e = tid; e < kD * kD; e += 128) Rs[e] = (e / kD == e % kD) ? 1.f : 0.f;
+    }
     const uint16_t* X = isV ? V : K;
     for (int e = tid; e < kAppTok * kD; e += 128) {
       const int r = e / kD, c = e % kD;
@@ -105,10 +110,14 @@ __global__ void __launch_bounds__(128) append_small_kernel(const uint16_t* __res
   const uint16_t* X = isV ? V : K;
   xs[c] = bf16_to_f32(X[((int64_t)t * ep.hkv + h) * kD + c]);
   __syncthreads();
-  const float* R = (isV ? RV : RK) + (size_t)h * kD * kD + c;
-  float acc = 0.f;
+  const float* Rb = isV ? RV : RK;        // R_V = NULL: pre-rotated V (NEXT-2) -> identity
+  float acc = xs[c];
+  if (Rb) {
+    const float* R = Rb + (size_t)h * kD * kD + c;
+    acc = 0.f;
 #pragma unroll 32
-  for (int k = 0; k < kD; ++k) acc = fmaf(xs[k], R[(size_t)k * kD], acc);
+    for (int k = 0; k < kD; ++k) acc = fmaf(xs[k], R[(size_t)k * kD], acc);
+  }
   ys[c] = acc;
   __syncthreads();
   if (c < 32) {
@@ -118,7 +127,7 @@ __global__ void __launch_bounds__(128) append_small_kernel(const uint16_t* __res
   }
 }
 
-bool append_small_ok(const oscar_ctx& c, int64_t T) { return T <= kSmallAppendMaxT && c.bits != 3; }
+bool append_small_ok(const oscar_ctx& c, int64_t T) { return T <= kSmallAppendMaxT; }
 
 cudaError_t launch_append_small(const oscar_ctx& c, const void* K, const void* V, const int64_t* slots,
                                 int64_t T, const float* RK, const float* RV, void* pool, cudaStream_t s) {

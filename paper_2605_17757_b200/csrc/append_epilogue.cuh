@@ -61,7 +61,7 @@ __device__ __forceinline__ float warp_row_rank_select(const float a[4], int k) {
   return tau;
 }
 
-// One warp owns one row: lane holds channels 4*lane .. 4*lane+3 in y[] (bits in {2, 4}).
+// One warp owns one row: lane holds channels 4*lane .. 4*lane+3 in y[] (bits in {2, 3, 4}).
 __device__ __forceinline__ void quantize_store_row_warp(const EpiParams& ep, float y[4], int lane,
                                                         int64_t slot, int h, int isV,
                                                         uint8_t* __restrict__ pool) {
@@ -90,17 +90,24 @@ __device__ __forceinline__ void quantize_store_row_warp(const EpiParams& ep, flo
   const int64_t page = slot / ep.P;
   const int off = (int)(slot % ep.P);
   uint8_t* blk = pool + (page * ep.hkv + h) * (int64_t)ep.page_bytes;
-  const int nbytes = ep.bits / 2;            // bytes per lane-chunk (4 codes)
-  const uint32_t chunk = ep.bits == 2
-      ? (uint32_t)(c[0] | (c[1] << 2) | (c[2] << 4) | (c[3] << 6))
-      : (uint32_t)(c[0] | (c[1] << 4) | (c[2] << 8) | (c[3] << 12));
+  // reading Z22 bitstream: this lane's 4 codes are bits [4·b·lane, 4·b·lane + 4b); byte j of the
+  // row (bits 8j .. 8j+7) lies in the fields of lanes a = 8j/(4b) and a + 1 (b = 3 straddles)
+  const int fb = 4 * ep.bits;                // bits per lane field
+  const uint32_t field = (uint32_t)c[0] | ((uint32_t)c[1] << ep.bits) | ((uint32_t)c[2] << (2 * ep.bits)) |
+                         ((uint32_t)c[3] << (3 * ep.bits));
+  const int rb = ep.row_bytes;
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    if (k >= nbytes) break;
-    const int j = lane * nbytes + k;         // byte index inside the row
-    const uint8_t v = (uint8_t)(chunk >> (8 * k));
-    if (!isV) blk[fmt_krow(off) * ep.row_bytes + j] = v;
-    else blk[ep.vcodes_off + fmt_vbyte(off, j, ep.row_bytes)] = v;
+  for (int m = 0; m < 2; ++m) {
+    const int j = lane + 32 * m;             // byte index inside the row
+    const int a = min((8 * j) / fb, 31);
+    const uint32_t lo = __shfl_sync(0xffffffffu, field, a);
+    const uint32_t hi = __shfl_sync(0xffffffffu, field, min(a + 1, 31));
+    const uint32_t both = lo | (hi << fb);
+    const uint8_t v = (uint8_t)(both >> (8 * j - fb * a));
+    if (j < rb) {
+      if (!isV) blk[fmt_krow(off) * rb + j] = v;
+      else blk[ep.vcodes_off + fmt_vbyte(off, j, rb)] = v;
+    }
   }
   if ((lane % lanes_per_group) == 0) {
     const int grp = lane / lanes_per_group;

@@ -135,14 +135,17 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
 
   // ---- R -> bf16 hi/lo, transposed to K-major (row n = output channel, k contiguous), SW128
   {
-    const float* R = (isV ? p.RV : p.RK) + (size_t)h * kD * kD;
+    // R_V = NULL: pre-rotated V (NEXT-2) -> identity (exact in bf16: R_lo = 0)
+    const float* Rb = isV ? p.RV : p.RK;
+    const float* R = Rb ? Rb + (size_t)h * kD * kD : nullptr;
     for (int idx = threadIdx.x; idx < kD * 16; idx += kThreads) {
       const int n = idx & 127, kc16 = idx >> 7;            // 16 chunks of 8 k
       uint32_t hi[4], lo[4];
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const float r0 = R[(size_t)(8 * kc16 + 2 * e) * kD + n];
-        const float r1 = R[(size_t)(8 * kc16 + 2 * e + 1) * kD + n];
+        const int k0 = 8 * kc16 + 2 * e, k1 = k0 + 1;
+        const float r0 = R ? R[(size_t)k0 * kD + n] : (k0 == n ? 1.f : 0.f);
+        const float r1 = R ? R[(size_t)k1 * kD + n] : (k1 == n ? 1.f : 0.f);
         const __nv_bfloat16 h0 = __float2bfloat16_rn(r0), h1 = __float2bfloat16_rn(r1);
         const __nv_bfloat16 l0 = __float2bfloat16_rn(r0 - __bfloat162float(h0));
         const __nv_bfloat16 l1 = __float2bfloat16_rn(r1 - __bfloat162float(h1));

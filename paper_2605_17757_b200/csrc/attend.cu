@@ -164,8 +164,10 @@ __global__ void __launch_bounds__(128) attend_partial_simple(AttnParams p) {
         for (int grp = 0; grp < p.ng; ++grp) {
           float dot = 0.f;
           for (int c = grp * p.G; c < (grp + 1) * p.G; ++c) {
-            const int bit = c * p.bits;
-            const int code = (krow[bit >> 3] >> (bit & 7)) & qmax;
+            const int bit = c * p.bits, jb = bit >> 3, sh = bit & 7;
+            int word = krow[jb];
+            if (sh + p.bits > 8) word |= krow[jb + 1] << 8;   // 3-bit codes straddle bytes
+            const int code = (word >> sh) & qmax;
             dot = fmaf(qs[i * kD + c], (float)code, dot);
           }
           const __half* mt = reinterpret_cast<const __half*>(meta + fmt_meta(t, grp, p.ng));
@@ -208,7 +210,9 @@ __global__ void __launch_bounds__(128) attend_partial_simple(AttnParams p) {
       const int jb = bit >> 3, sh = bit & 7;
       for (int i = 0; i < g; ++i) acc[i] *= alpha[i];
       for (int t = 0; t < valid; ++t) {
-        const int code = (pg[p.vcodes_off + fmt_vbyte(t, jb, rb)] >> sh) & qmax;
+        int word = pg[p.vcodes_off + fmt_vbyte(t, jb, rb)];
+        if (sh + p.bits > 8) word |= pg[p.vcodes_off + fmt_vbyte(t, jb + 1, rb)] << 8;
+        const int code = (word >> sh) & qmax;
         const __half* mt = reinterpret_cast<const __half*>(meta + fmt_meta(t, grp, p.ng) + 16);
         const float v = fmaf(__half2float(mt[0]), (float)code, __half2float(mt[1]));
         for (int i = 0; i < g; ++i) acc[i] = fmaf(sc[i * P + t], v, acc[i]);
@@ -293,13 +297,17 @@ __global__ void __launch_bounds__(512) attend_merge_kernel(AttnParams p, const f
   }
   __syncthreads();
   const float4 o4 = reinterpret_cast<const float4*>(ot)[lane];
-  const float* R = RV + (size_t)h * kD * kD;
   const float sw = bc[2];
 #pragma unroll 4
   for (int cp = w; cp < kD; cp += 16) {
-    const float4 r4 = reinterpret_cast<const float4*>(R + (size_t)cp * kD)[lane];
-    float v = r4.x * o4.x + r4.y * o4.y + r4.z * o4.z + r4.w * o4.w;
-    for (int of = 16; of > 0; of >>= 1) v += __shfl_xor_sync(0xffffffffu, v, of);
+    float v;
+    if (RV) {
+      const float4 r4 = reinterpret_cast<const float4*>(RV + (size_t)h * kD * kD + (size_t)cp * kD)[lane];
+      v = r4.x * o4.x + r4.y * o4.y + r4.z * o4.z + r4.w * o4.w;
+      for (int of = 16; of > 0; of >>= 1) v += __shfl_xor_sync(0xffffffffu, v, of);
+    } else {
+      v = ot[cp];                       // pre-rotated V (NEXT-2): õ is already in V's frame
+    }
     if (lane == 0) {
       if (seg) v += p.seg_o[(size_t)row * kD + cp] * sw;
       const size_t idx = (size_t)row * kD + cp;

@@ -10,8 +10,9 @@
 // finishes).  Per page, in chunks of up to 64 tokens:
 //   QK  : IMMA m16n8k32 s8 x u8 -> s32.  A = q̃ quantized to 15 bits and split hi/lo int8
 //         (rows = (hi|lo) x (group, head) "combos", zero outside the combo's group; built once
-//         per (b, h) by q_rotate_kernel), B = the raw 2/4-bit codes expanded to bytes with one
-//         SHF + LOP3 per 4 codes.  Exact integer dots per (token, head, group); the fp32
+//         per (b, h) by q_rotate_kernel), B = the raw 2/4-bit codes moved to the top bits of
+//         each byte (a left shift = IMAD on the FMA pipe, + one LOP3 per 4 codes; the 2^(8-b)
+//         byte scale is folded into qscale / qsum).  Exact integer dots per (token, head, group); the fp32
 //         epilogue applies s_K, m_K (x̂ = s·c + m).
 //   soft: online softmax in the log2 domain, one max per 64-token chunk; the running max
 //         follows every increase (OSCAR_LAZY = 0), so the dominant token's weight is exactly
@@ -30,9 +31,6 @@ namespace oscar {
 namespace {
 
 constexpr int kWarps = 4;
-#ifndef OSCAR_QK_LSHIFT
-#define OSCAR_QK_LSHIFT 0
-#endif
 #ifndef OSCAR_CHUNK
 #define OSCAR_CHUNK 4
 #endif
@@ -206,13 +204,8 @@ attend_partial_mma(AttnParams p, int S) {
   while (cur < n_items) {
     const Item I = decode_item(p, cur);
     const size_t qrow = (size_t)I.b * p.hq + (size_t)I.h * GQ + hh;
-#if OSCAR_QK_LSHIFT
     constexpr float kBScale = (float)(1 << (8 - BITS));   // B bytes carry c·2^(8-BITS)
     const float qscale = real ? p.qscale[qrow] * (1.f / kBScale) : 0.f;
-#else
-    constexpr float kBScale = 1.f;
-    const float qscale = real ? p.qscale[qrow] : 0.f;
-#endif
     int grp_of[NT];
     float qsumf[NT];
 #pragma unroll
@@ -286,7 +279,6 @@ attend_partial_mma(AttnParams p, int S) {
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {
               uint32_t b0, b1;
-#if OSCAR_QK_LSHIFT
               // codes moved to the top bits of each byte with a left shift (a multiply: FMA
               // pipe) and one mask: every B byte is c·2^(8-BITS), folded into qscale
               constexpr uint32_t kTopMask = kByteMask << (8 - BITS);
@@ -297,15 +289,6 @@ attend_partial_mma(AttnParams p, int S) {
                 b0 = (w[kk >> 1] * (1u << (4 - 4 * (kk & 1)))) & kTopMask;
                 b1 = (w[2 + (kk >> 1)] * (1u << (4 - 4 * (kk & 1)))) & kTopMask;
               }
-#else
-              if (BITS == 2) {
-                b0 = (w[0] >> (2 * kk)) & kByteMask;
-                b1 = (w[1] >> (2 * kk)) & kByteMask;
-              } else {
-                b0 = (w[kk >> 1] >> (4 * (kk & 1))) & kByteMask;
-                b1 = (w[2 + (kk >> 1)] >> (4 * (kk & 1))) & kByteMask;
-              }
-#endif
 #pragma unroll
               for (int j = 0; j < NT; ++j) imma16832(cq[j][nt], aq[j][kk], b0, b1);
             }

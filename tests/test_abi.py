@@ -57,7 +57,7 @@ def test_create_validation():
     from paper_2605_17757_b200 import binding as B
     bad = [(dict(head_dim=96), B.ERR_DIM), (dict(head_dim=64), B.ERR_UNSUPPORTED),
            (dict(num_q_heads=30), B.ERR_ARG), (dict(bits=5), B.ERR_ARG),
-           (dict(bits=3), B.ERR_UNSUPPORTED), (dict(group_size=48), B.ERR_ARG),
+           (dict(group_size=48), B.ERR_ARG),
            (dict(page_size=20), B.ERR_ARG), (dict(clip_ratio_k=0.0), B.ERR_ARG),
            (dict(clip_ratio_v=1.5), B.ERR_ARG), (dict(num_q_heads=72, num_kv_heads=8), B.ERR_UNSUPPORTED)]
     for kw, st in bad:
@@ -73,7 +73,7 @@ def test_page_bytes_matches_format():
     B, o = _ctx(bits=4, group_size=32, page_size=64, num_q_heads=1, num_kv_heads=1)
     assert o.page_bytes() == 2 * 64 * 64 + 64 * 4 * 8
     import oracle as O
-    for bits, G, P in [(2, 64, 64), (4, 32, 64), (2, 128, 16), (4, 64, 32)]:
+    for bits, G, P in [(2, 64, 64), (4, 32, 64), (2, 128, 16), (4, 64, 32), (3, 64, 64), (3, 32, 16)]:
         B, o = _ctx(bits=bits, group_size=G, page_size=P)
         assert o.page_bytes() == O.PageFormat(128, bits, G, P).page_bytes
 

@@ -111,6 +111,8 @@ def _slots(rng, mode, Tn, npages):
     (4, 64, (1.0, 1.0), 0, 300, "perm"), (4, 32, (1.0, 1.0), 0, 1280, "perm"),
     (2, 128, (1.0, 1.0), 0, 129, "perm"),
     (2, 64, (1.0, 1.0), 0, 1000, "contig208"), (4, 64, (1.0, 1.0), 0, 1000, "contig208"),
+    (3, 64, (1.0, 1.0), 0, 1000, "perm"), (3, 32, (0.96, 0.92), 0, 300, "contig208"),
+    (3, 128, (1.0, 1.0), 0, 40, "perm"),
     (2, 32, (1.0, 1.0), 0, 1000, "contig200"), (4, 32, (1.0, 1.0), 0, 1280, "contig0"),
 ])
 def test_quantize_append_parity(bits, G, rho, variant, Tn, slot_mode):
@@ -180,6 +182,7 @@ def _run_attend(o, q, pt, L, pool, RK, RV):
     dict(name="g2b4", Hq=4, Hkv=2, bits=4, G=64, B=2, L=[300, 1]),
     dict(name="C4small", Hq=16, Hkv=2, bits=2, G=64, B=2, L=[700, 130]),     # g=8, two 8-combo tiles
     dict(name="g4G32", Hq=8, Hkv=2, bits=4, G=32, B=2, L=[450, 64]),        # 4 groups x 4 heads
+    dict(name="b3", Hq=8, Hkv=2, bits=3, G=64, B=2, L=[333, 64]),           # 3-bit: simple kernels
 ])
 @pytest.mark.parametrize("variant", [0, 1])
 @pytest.mark.parametrize("pps", [0, 1, 3])

@@ -9,6 +9,10 @@
 #include "common.cuh"
 #include "attend_common.cuh"
 
+#ifndef OSCAR_PDL_MERGE
+#define OSCAR_PDL_MERGE 1
+#endif
+
 namespace oscar {
 
 // ------------------------------------------------------------------ q rotation
@@ -506,7 +510,7 @@ cudaError_t launch_attend(const oscar_ctx& c, const void* q, const int32_t* page
     cfg.dynamicSmemBytes = msmem;
     cfg.stream = s;
     cfg.attrs = pdl;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = OSCAR_PDL_MERGE;
     e = cudaLaunchKernelEx(&cfg, attend_merge_kernel, p, RV, out, out_fp32, lse);
     if (e != cudaSuccess) return e;
   }

@@ -70,6 +70,40 @@ __device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
+// packed fp32x2 arithmetic (FFMA2 / FMUL2 / FADD2: one issue slot for two lanes of math)
+struct f2 { float x, y; };
+__device__ __forceinline__ uint64_t f2_u64(f2 a) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a.x), "f"(a.y));
+  return r;
+}
+__device__ __forceinline__ f2 u64_f2(uint64_t r) {
+  f2 a;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(r));
+  return a;
+}
+__device__ __forceinline__ f2 ffma2(f2 a, f2 b, f2 c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2_u64(a)), "l"(f2_u64(b)), "l"(f2_u64(c)));
+  return u64_f2(r);
+}
+__device__ __forceinline__ f2 fmul2(f2 a, f2 b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_u64(a)), "l"(f2_u64(b)));
+  return u64_f2(r);
+}
+__device__ __forceinline__ f2 fadd2(f2 a, f2 b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_u64(a)), "l"(f2_u64(b)));
+  return u64_f2(r);
+}
+// (low halves, high halves) of two half2 words as fp32 pairs
+__device__ __forceinline__ void halves_f2(uint32_t w0, uint32_t w1, f2& lo, f2& hi) {
+  const __half2 a = *reinterpret_cast<const __half2*>(&w0), b = *reinterpret_cast<const __half2*>(&w1);
+  lo = f2{__low2float(a), __low2float(b)};
+  hi = f2{__high2float(a), __high2float(b)};
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -225,10 +259,10 @@ attend_partial_mma(AttnParams p, int S) {
           for (int r = 0; r < 4; ++r) aq[j][kk][r] = qf[(j * 16 + kk * 4 + r) * 32];
     }
     float acc[8][NT][4];
-    float mv_acc[NT];                         // Σ p·m_V of this lane's combo over its tokens
+    f2 mv2[NT];                               // Σ p·m_V of this lane's combo over its tokens (2 partial sums)
 #pragma unroll
     for (int j = 0; j < NT; ++j) {
-      mv_acc[j] = 0.f;
+      mv2[j] = f2{0.f, 0.f};
 #pragma unroll
       for (int e = 0; e < 4; ++e)
 #pragma unroll
@@ -236,7 +270,8 @@ attend_partial_mma(AttnParams p, int S) {
     }
     // scores are kept relative to m_run (log2 domain); m_run starts at 0 and the first chunk
     // of the item moves it to that chunk's max, later chunks only when the max grows by > 8
-    float m_run = 0.f, l_run = 0.f;
+    float m_run = 0.f;
+    f2 l2{0.f, 0.f};                          // Σ p of this lane's tokens (2 partial sums)
     bool fresh = true;
 
     // one page: chunks of up to 4 sub-tiles (64 tokens)
@@ -293,29 +328,42 @@ attend_partial_mma(AttnParams p, int S) {
               for (int j = 0; j < NT; ++j) imma16832(cq[j][nt], aq[j][kk], b0, b1);
             }
           }
-          // ---- scores of tokens 4t + e for head hh (log2 domain, relative to m_run)
-          float part[4] = {0.f, 0.f, 0.f, 0.f};
+          // ---- scores of tokens 4t + e for head hh (log2 domain, relative to m_run), as the
+          // pairs e = (0, 1) and (2, 3)
+          f2 part[2] = {{0.f, 0.f}, {0.f, 0.f}};
 #pragma unroll
           for (int j = 0; j < NT; ++j) {
             const uint4 mk4 = *reinterpret_cast<const uint4*>(meta + 128 * NG * st + 128 * grp_of[j] + 32 * t);
             const uint32_t mw[4] = {mk4.x, mk4.y, mk4.z, mk4.w};
+            const f2 qs2{qsumf[j], qsumf[j]};
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int nt = e & 1, col = e >> 1;   // token 4t+e <-> (N-tile e&1, column 2t + e/2)
-              const int dot = cq[j][nt][col] * 256 + cq[j][nt][2 + col];
-              const __half2 smk = *reinterpret_cast<const __half2*>(&mw[e]);
-              part[e] = fmaf(__low2float(smk), (float)dot, fmaf(__high2float(smk), qsumf[j], part[e]));
+            for (int pe = 0; pe < 2; ++pe) {
+              // token 4t+e <-> (N-tile e&1, column 2t + e/2): e = 2pe (nt 0), 2pe+1 (nt 1), col = pe
+              const int d0 = cq[j][0][pe] * 256 + cq[j][0][2 + pe];
+              const int d1 = cq[j][1][pe] * 256 + cq[j][1][2 + pe];
+              f2 sk, mk;
+              halves_f2(mw[2 * pe], mw[2 * pe + 1], sk, mk);
+              part[pe] = ffma2(sk, f2{(float)d0, (float)d1}, ffma2(mk, qs2, part[pe]));
             }
           }
 #pragma unroll
           for (int x = GQ; x < 8 && x < NC; x <<= 1)
 #pragma unroll
-            for (int e = 0; e < 4; ++e) part[e] += __shfl_xor_sync(0xffffffffu, part[e], x * 4);
+            for (int pe = 0; pe < 2; ++pe)
+              part[pe] = fadd2(part[pe], f2{__shfl_xor_sync(0xffffffffu, part[pe].x, x * 4),
+                                            __shfl_xor_sync(0xffffffffu, part[pe].y, x * 4)});
+          const f2 qsc{qscale, qscale}, nm{-m_run, -m_run};
+#pragma unroll
+          for (int pe = 0; pe < 2; ++pe) {
+            const f2 v = ffma2(part[pe], qsc, nm);
+            sc[sl][2 * pe] = v.x;
+            sc[sl][2 * pe + 1] = v.y;
+          }
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             bool ok = real;
             if (!FULL) ok = ok && (16 * st + 4 * t + e) < valid;
-            sc[sl][e] = ok ? fmaf(part[e], qscale, -m_run) : -INFINITY;
+            if (!ok) sc[sl][e] = -INFINITY;
             tmax = fmaxf(tmax, sc[sl][e]);
           }
         }
@@ -333,12 +381,12 @@ attend_partial_mma(AttnParams p, int S) {
 #pragma unroll
             for (int e = 0; e < 4; ++e) sc[sl][e] -= shift;
           m_run += shift;
-          l_run *= alpha;
+          l2 = fmul2(l2, f2{alpha, alpha});
           const float a0 = __shfl_sync(0xffffffffu, alpha, 8 * t);
           const float a1 = __shfl_sync(0xffffffffu, alpha, 8 * t + 4);
 #pragma unroll
           for (int j = 0; j < NT; ++j) {
-            mv_acc[j] *= alpha;
+            mv2[j] = fmul2(mv2[j], f2{alpha, alpha});
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
               acc[i][j][0] *= a0; acc[i][j][2] *= a0;
@@ -353,30 +401,26 @@ attend_partial_mma(AttnParams p, int S) {
           if (st >= n_sub) break;
           float pr[4];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            pr[e] = ex2_ftz(sc[sl][e]);            // exp2(-inf) = 0
-            l_run += pr[e];
-          }
+          for (int e = 0; e < 4; ++e) pr[e] = ex2_ftz(sc[sl][e]);   // exp2(-inf) = 0
+          const f2 p01{pr[0], pr[1]}, p23{pr[2], pr[3]};
+          l2 = fadd2(l2, fadd2(p01, p23));
           uint32_t bpv[NT][2];
 #pragma unroll
           for (int j = 0; j < NT; ++j) {
             const uint4 mv4 = *reinterpret_cast<const uint4*>(meta + 128 * NG * st + 128 * grp_of[j] + 32 * t + 16);
-            const uint32_t mw[4] = {mv4.x, mv4.y, mv4.z, mv4.w};
-            float w4[4];
+            uint32_t mw[4] = {mv4.x, mv4.y, mv4.z, mv4.w};
+            if (!FULL) {   // masked tokens may carry garbage metadata: keep them out
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              // p·s_V and p·m_V in fp32 (one fp16 rounding of the MMA operand; the m_V sum exact)
-              const __half2 smv = *reinterpret_cast<const __half2*>(&mw[e]);
-              if (FULL) {
-                w4[e] = pr[e] * __low2float(smv);
-                mv_acc[j] = fmaf(pr[e], __high2float(smv), mv_acc[j]);
-              } else {   // masked tokens may carry garbage metadata: keep them out
-                w4[e] = pr[e] == 0.f ? 0.f : pr[e] * __low2float(smv);
-                mv_acc[j] = pr[e] == 0.f ? mv_acc[j] : fmaf(pr[e], __high2float(smv), mv_acc[j]);
-              }
+              for (int e = 0; e < 4; ++e) mw[e] = pr[e] == 0.f ? 0u : mw[e];
             }
-            bpv[j][0] = pack_half2(w4[0], w4[2]);   // k-slots 2t, 2t+1 <-> tokens 4t, 4t+2
-            bpv[j][1] = pack_half2(w4[1], w4[3]);   // k-slots 2t+8, 2t+9 <-> tokens 4t+1, 4t+3
+            // p·s_V and p·m_V in fp32 (one fp16 rounding of the MMA operand; the m_V sum exact)
+            f2 s01, m01, s23, m23;
+            halves_f2(mw[0], mw[1], s01, m01);
+            halves_f2(mw[2], mw[3], s23, m23);
+            const f2 w01 = fmul2(p01, s01), w23 = fmul2(p23, s23);
+            mv2[j] = ffma2(p01, m01, ffma2(p23, m23, mv2[j]));
+            bpv[j][0] = pack_half2(w01.x, w23.x);   // k-slots 2t, 2t+1 <-> tokens 4t, 4t+2
+            bpv[j][1] = pack_half2(w01.y, w23.y);   // k-slots 2t+8, 2t+9 <-> tokens 4t+1, 4t+3
           }
           uint32_t vw[VW];
           {
@@ -420,10 +464,13 @@ attend_partial_mma(AttnParams p, int S) {
     }
 
     // ---- write this item's partial (unnormalized õ in the rotated frame, m, l)
+    float l_run = l2.x + l2.y;
     l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
     l_run += __shfl_xor_sync(0xffffffffu, l_run, 2);
+    float mv_acc[NT];
 #pragma unroll
     for (int j = 0; j < NT; ++j) {
+      mv_acc[j] = mv2[j].x + mv2[j].y;
       mv_acc[j] += __shfl_xor_sync(0xffffffffu, mv_acc[j], 1);
       mv_acc[j] += __shfl_xor_sync(0xffffffffu, mv_acc[j], 2);
     }

@@ -231,6 +231,7 @@ def main():
     ap.add_argument("--variant", type=int, default=0, help="0 = fastest kernels, 1 = simple reference kernels")
     ap.add_argument("--no-extras", action="store_true", help="skip calibration / prefill / e2e / cpu legs (ncu runs)")
     ap.add_argument("--no-c4", action="store_true", help="skip the C4 (Llama-3-70B-shaped, 128k) decode leg")
+    ap.add_argument("--c4-only", action="store_true", help="run only the C4 decode leg and print its dict")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -251,6 +252,14 @@ def main():
     from paper_2605_17757_b200.parallel import allreduce_covariances, barrier, max_over_ranks
 
     hbm_peak, _, peak_kind = measured_peaks()
+    if args.c4_only:
+        gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+        RK = torch.stack([synth.torch_rotation(gen, HKV, D, dev) for _ in range(C4_LAYERS)])
+        RV = torch.stack([synth.torch_rotation(gen, HKV, D, dev) for _ in range(C4_LAYERS)])
+        r = c4_leg(args, world, rank, dev, gen, RK, RV, hbm_peak, peak_kind)
+        if rank == 0:
+            print(json.dumps(r), flush=True)
+        return
     o = Bnd.Oscar(Bnd.Config(num_q_heads=HQ, num_kv_heads=HKV, bits=BITS, group_size=G, page_size=P))
     o.set_variant(args.variant)
     stream = torch.cuda.current_stream()

@@ -107,6 +107,20 @@ OSCAR_API oscar_status oscar_calib_finalize(const oscar_ctx* ctx, const double* 
                                   int64_t n_rows, float* R_K, float* R_V, double* evals,
                                   int32_t* info, void* stream);
 
+/* CalibrateClip (Alg. 1; the procedure is unspecified in the paper — reading Z34 follows
+ * SPEC S:L152-160): for each KV head h and each candidate ratio rho_g of `grid`, the frozen-error
+ * surrogates of Theorem 1 of clip + quantize at rho_g,
+ *   obj[h][0][g] = tr(R_K[h]ᵀ C_Q[h] R_K[h] · E_K),  E_K = Σ_j e_jᵀ e_j,
+ *   e_j = dequant(quant(clip(k_j R_K[h], rho_g))) − k_j R_K[h]            (App A.5, ctx bits / G)
+ * and obj[h][1][g] likewise for V with R_V and C_S.  K, V: bf16 [N][H_kv][d] calibration rows;
+ * R_K, R_V: fp32 [H_kv][d][d]; acc: fp64 [H_kv][2][d][d] (C_Q, C_S sums of calib_accumulate;
+ * the normalization does not change the argmin); grid: host float[n_grid], values in (0, 1],
+ * 1 <= n_grid <= 16; obj: device fp64 [H_kv][2][n_grid] (overwritten).  The per-layer choice is
+ * argmin_g Σ_h obj[h][side][g] (binding: Oscar.calib_clip).  N = 0 -> obj = 0. */
+OSCAR_API oscar_status oscar_calib_clip(const oscar_ctx* ctx, const void* K, const void* V, int64_t N,
+                              const float* R_K, const float* R_V, const double* acc,
+                              const float* grid, int32_t n_grid, double* obj, void* stream);
+
 /* ---------------------------------------------------------------- quantize_append(K, V)
  * For each of the T rows and each KV head h: x̃ = x·R_h (K with R_K, V with R_V), per-token
  * percentile clip (rho from the config), per-(token, group) min-max quantization to b-bit

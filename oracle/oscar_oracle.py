@@ -20,6 +20,7 @@ __all__ = [
     "clip_rows", "quantize_rows", "dequantize_rows", "pack_codes", "unpack_codes",
     "PageFormat", "quantize_rotated", "quantize_append", "read_rows", "attend_rows",
     "attend", "attend_mixed", "attend_alg1", "residual_cov", "group_ranges", "effective_bpe",
+    "clip_objectives", "calibrate_clip",
 ]
 
 
@@ -188,11 +189,11 @@ def clip_rows(Xr: np.ndarray, rho: float) -> np.ndarray:
 # App A.5: per-token, per-group asymmetric min-max quantizer,
 # q_max = 2^b - 1, s = (max - min)/q_max, Q+ = clip(round(x/s + z), 0, q_max).
 # Reading Z2/Z3/Z4: store (s16, m16) = fp16_rne(s), fp16_rne(min) (m = -s·z), and
-# compute codes from the STORED metadata in fp32 with this exact operation order:
+# compute codes from the STORED metadata with this exact operation order:
 #   s = (mx - mn) / q_max          [fp32 sub RN, fp32 div RN]
 #   inv = 1 / float(s16)  (0 if s16 == 0)
-#   t = (x - float(m16)) * inv      [fp32 sub RN, fp32 mul RN, no FMA]
-#   c = clamp(rint_half_even(t), 0, q_max)      (reading Z1)
+#   dx = x - float(m16)             [fp32 sub RN]
+#   c = clamp(rint_half_even(dx·inv exactly), 0, q_max)      (readings Z1, Z4)
 # Returns codes uint8 [..., d], s16, m16 float16 [..., d/G].
 # ----------------------------------------------------------------------------------
 def quantize_rows(Xc: np.ndarray, bits: int, G: int):
@@ -491,3 +492,39 @@ def effective_bpe(bits: int, G: int, sink_recent: int = 0, L: int = 1, meta_bits
         raise ValueError("L must exceed sink+recent")
     f = sink_recent / L if sink_recent else 0.0
     return (1.0 - f) * (bits + meta_bits / G) + 16.0 * f
+
+
+# ----------------------------------------------------------------------------------
+# Alg. 1 `CalibrateClip` (outputs c_K, c_V by reading Z17).  The paper does not
+# specify the procedure; reading Z34: exhaustive search over a grid
+# of clip ratios for the frozen-error surrogates of Theorem 1 (App A.6):
+#   L_K(rho) = tr(R_K^T C_Q R_K E_K(rho)),  E_K(rho) = sum_j e_j^T e_j,
+#   e_j = Q(clip(k_j R_K, rho)) - k_j R_K         (App A.5 clip + quantize)
+# and L_V with (R_V, C_S, V).  One ratio pair per layer: the grid entry minimizing the sum over
+# KV heads (S:L190 per-layer default); ties go to the earlier grid entry.
+# ----------------------------------------------------------------------------------
+def clip_objectives(X: np.ndarray, R: np.ndarray, C: np.ndarray, grid, bits: int, G: int) -> np.ndarray:
+    """X [N, d] raw rows of one KV head, R [d, d], C [d, d] covariance target.  Returns the
+    surrogate tr(R^T C R E(rho)) for each rho of the grid (fp64)."""
+    Xr = rotate(np.asarray(X)[:, None, :], np.asarray(R)[None])[:, 0]   # fp32 rotated rows
+    M = np.asarray(R, np.float64).T @ np.asarray(C, np.float64) @ np.asarray(R, np.float64)
+    out = np.zeros(len(grid))
+    for i, rho in enumerate(grid):
+        Xc = clip_rows(Xr, rho)
+        codes, s16, m16 = quantize_rows(Xc, bits, G)
+        e = dequantize_rows(codes, s16, m16, G) - Xr.astype(np.float64)
+        E = e.T @ e                                       # frozen residual covariance
+        out[i] = np.trace(M @ E)
+    return out
+
+
+def calibrate_clip(K, V, R_K, R_V, C_Q, C_S, grid, bits: int, G: int):
+    """K, V [N, H_kv, d]; R_* [H_kv, d, d]; C_* [H_kv, d, d].  Returns (obj [H_kv, 2, n_grid],
+    rho_K, rho_V)."""
+    H = K.shape[1]
+    obj = np.zeros((H, 2, len(grid)))
+    for h in range(H):
+        obj[h, 0] = clip_objectives(K[:, h], R_K[h], C_Q[h], grid, bits, G)
+        obj[h, 1] = clip_objectives(V[:, h], R_V[h], C_S[h], grid, bits, G)
+    tot = obj.sum(axis=0)
+    return obj, float(grid[int(np.argmin(tot[0]))]), float(grid[int(np.argmin(tot[1]))])

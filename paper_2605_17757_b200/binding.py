@@ -24,7 +24,7 @@ EXPORTED = [
     "oscar_create", "oscar_destroy", "oscar_last_error", "oscar_version", "oscar_page_bytes",
     "oscar_calib_accumulate", "oscar_calib_finalize", "oscar_quantize_append",
     "oscar_attend_workspace_bytes", "oscar_attend", "oscar_attend_mixed", "oscar_rotate",
-    "oscar_quantize_rotated", "oscar_set_variant",
+    "oscar_quantize_rotated", "oscar_set_variant", "oscar_calib_clip",
 ]
 
 
@@ -56,6 +56,8 @@ _sig = {
     "oscar_rotate": (_i32, [_vp, _vp, _vp, _vp, _i64, _vp]),
     "oscar_quantize_rotated": (_i32, [_vp, _vp, _vp, _vp, _i64, _vp, _vp]),
     "oscar_set_variant": (_i32, [_vp, _i32]),
+    "oscar_calib_clip": (_i32, [_vp, _vp, _vp, _i64, _vp, _vp, _vp, ctypes.POINTER(ctypes.c_float), _i32, _vp,
+                                _vp]),
 }
 for _name, (_res, _args) in _sig.items():
     _f = getattr(_lib, _name)
@@ -140,6 +142,20 @@ class Oscar:
         _check(_lib.oscar_calib_finalize(self._h, _ptr(acc), n_mats, n_rows, _ptr(R_K), _ptr(R_V),
                                          _ptr(evals), _ptr(info), _stream(stream)),
                "oscar_calib_finalize")
+
+    def calib_clip(self, K, V, R_K, R_V, acc, grid, obj=None, stream=None):
+        """CalibrateClip (reading Z34): surrogate objectives obj [H_kv, 2, n_grid] (fp64, device)
+        and the per-layer choice (rho_K, rho_V) = argmin over the grid of the sum over KV heads
+        (first grid entry on ties).  Synchronizes to read the objectives back."""
+        import torch
+        n = len(grid)
+        if obj is None:
+            obj = torch.empty((self.cfg.num_kv_heads, 2, n), dtype=torch.float64, device=K.device)
+        g = (ctypes.c_float * n)(*[float(x) for x in grid])
+        _check(_lib.oscar_calib_clip(self._h, _ptr(K), _ptr(V), K.shape[0], _ptr(R_K), _ptr(R_V), _ptr(acc),
+                                     g, n, _ptr(obj), _stream(stream)), "oscar_calib_clip")
+        tot = obj.sum(dim=0).cpu()
+        return obj, float(grid[int(torch.argmin(tot[0]))]), float(grid[int(torch.argmin(tot[1]))])
 
     # ---------------------------------------------------------------- quantize_append
     def quantize_append(self, K, V, slots, R_K, R_V, pool, stream=None):

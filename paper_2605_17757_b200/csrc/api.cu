@@ -126,6 +126,26 @@ oscar_status oscar_calib_accumulate(const oscar_ctx* ctx, const void* Q, const v
   return cuda_status(oscar::launch_cov_accum(*ctx, Q, SV, N, acc, as_stream(stream)), "cov_accum");
 }
 
+oscar_status oscar_calib_clip(const oscar_ctx* ctx, const void* K, const void* V, int64_t N,
+                              const float* R_K, const float* R_V, const double* acc,
+                              const float* grid, int32_t n_grid, double* obj, void* stream) {
+  if (!ctx) return fail(OSCAR_ERR_ARG, "NULL ctx");
+  if (N < 0) return fail(OSCAR_ERR_ARG, "N must be >= 0 (got %lld)", (long long)N);
+  if (!grid || n_grid < 1 || n_grid > oscar::kMaxClipGrid)
+    return fail(OSCAR_ERR_ARG, "grid must hold 1..%d ratios", oscar::kMaxClipGrid);
+  if (!obj) return fail(OSCAR_ERR_ARG, "oscar_calib_clip: NULL obj");
+  int32_t kidx[oscar::kMaxClipGrid];
+  for (int g = 0; g < n_grid; ++g) {
+    if (!(grid[g] > 0.f && grid[g] <= 1.f)) return fail(OSCAR_ERR_ARG, "clip ratios must be in (0, 1]");
+    kidx[g] = (int32_t)std::ceil((double)grid[g] * ctx->d) - 1;     // reading Z6 nearest rank
+  }
+  cudaStream_t s = as_stream(stream);
+  if (N == 0)
+    return cuda_status(cudaMemsetAsync(obj, 0, sizeof(double) * ctx->hkv * 2 * n_grid, s), "calib_clip");
+  if (!K || !V || !R_K || !R_V || !acc) return fail(OSCAR_ERR_ARG, "oscar_calib_clip: NULL pointer");
+  return cuda_status(oscar::launch_calib_clip(*ctx, K, V, N, R_K, R_V, acc, kidx, n_grid, obj, s), "calib_clip");
+}
+
 oscar_status oscar_calib_finalize(const oscar_ctx* ctx, const double* acc, int32_t n_mats,
                                   int64_t n_rows, float* R_K, float* R_V, double* evals,
                                   int32_t* info, void* stream) {

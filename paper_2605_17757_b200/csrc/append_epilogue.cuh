@@ -1,8 +1,8 @@
 // Clip + per-group min-max quantize + pack + store of one rotated row (App A.5, P:L1235-1311;
 // Alg. 1 QuantizeAndWrite P:L1639-1643).  Operation order = reading Z4:
 //   s = (mx - mn) / q_max [fp32 RN]; s16 = fp16_rn(s); m16 = fp16_rn(mn);
-//   inv = s16 > 0 ? 1 / float(s16) : 0; t = (x - float(m16)) * inv [RN, RN, no FMA];
-//   c = clamp(rint(t), 0, q_max).
+//   inv = s16 > 0 ? 1 / float(s16) : 0; dx = x - float(m16) [RN];
+//   c = clamp(rint(dx·inv, product exact), 0, q_max).
 #pragma once
 #include "common.cuh"
 

@@ -34,7 +34,12 @@ constexpr int kWarps = 4;
 #ifndef OSCAR_CHUNK
 #define OSCAR_CHUNK 4
 #endif
-constexpr int kChunk = OSCAR_CHUNK;       // 16-token sub-tiles per softmax chunk
+#ifndef OSCAR_CHUNK_NT2
+#define OSCAR_CHUNK_NT2 4
+#endif
+#ifndef OSCAR_MINB_NT2
+#define OSCAR_MINB_NT2 3
+#endif
 #ifndef OSCAR_LAZY
 #define OSCAR_LAZY 0
 #endif
@@ -162,10 +167,11 @@ __device__ __forceinline__ Item decode_item(const AttnParams& p, int it) {
 }  // namespace
 
 template <int BITS, int GQ, int NG>
-__global__ void __launch_bounds__(kWarps * 32, (GQ * NG <= 8 ? OSCAR_MINB : 3))
+__global__ void __launch_bounds__(kWarps * 32, (GQ * NG <= 8 ? OSCAR_MINB : OSCAR_MINB_NT2))
 attend_partial_mma(AttnParams p, int S) {
   constexpr int NC = GQ * NG;                 // (group, head) combos
   constexpr int NT = (NC + 7) / 8;            // 8-combo tiles (QK M-tiles / PV N-tiles)
+  constexpr int kChunk = NT > 1 ? OSCAR_CHUNK_NT2 : OSCAR_CHUNK;   // 16-token sub-tiles per softmax chunk
   constexpr int RB = 16 * BITS;               // packed row bytes (d = 128)
   constexpr int G = 128 / NG;
   constexpr int CPB = 8 / BITS;

@@ -28,6 +28,11 @@ constexpr float kLog2e = 1.4426950408889634f;
 // calib.cu
 cudaError_t launch_cov_accum(const oscar_ctx& c, const void* Q, const void* SV, int64_t N,
                              double* acc, cudaStream_t s);
+// clip.cu (CalibrateClip surrogate objectives, reading Z34)
+constexpr int kMaxClipGrid = 16;
+cudaError_t launch_calib_clip(const oscar_ctx& c, const void* K, const void* V, int64_t N,
+                              const float* RK, const float* RV, const double* acc,
+                              const int32_t* kidx, int n_grid, double* obj, cudaStream_t s);
 cudaError_t launch_jacobi_compose(const oscar_ctx& c, const double* acc, int n_mats,
                                   double inv_rows, float* RK, float* RV, double* evals,
                                   int32_t* info, cudaStream_t s);

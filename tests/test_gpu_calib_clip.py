@@ -1,0 +1,60 @@
+"""GPU parity of CalibrateClip (Alg. 1, reading Z34): the frozen-error surrogate
+objectives tr(Rᵀ C R E(rho)) per (KV head, side, rho) against the fp64 oracle, and the per-layer
+choice.  The GPU rotates in fp32 (the oracle in fp64, rounded to fp32), so an occasional code
+differs at a rounding boundary: objectives are compared at 1e-3 relative."""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2605_17757_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+GRID = [0.88, 0.92, 0.96, 0.98, 1.0]      # Table 10 grid
+
+
+def T(x, dtype=None):
+    import torch
+    t = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    return t.to(dtype) if dtype is not None else t
+
+
+@pytest.mark.parametrize("bits,G,N", [(2, 64, 1500), (4, 32, 700), (3, 64, 300)])
+def test_calib_clip_parity(bits, G, N):
+    import torch
+    from paper_2605_17757_b200 import binding as B
+    rng = np.random.default_rng(11 + bits + N)
+    Hq, H = 8, 2
+    K = synth.gen_keys(rng, N, H, 128)
+    V = synth.gen_values(rng, N, H, 128)
+    Q = synth.gen_queries(rng, N, Hq, H, 128)
+    SV = synth.gen_sv(rng, N, Hq, 128)
+    acc = np.stack([O.cov_accumulate(Q, H), O.cov_accumulate(SV, H)], axis=1)    # [H, 2, d, d]
+    RK, RV = synth.gen_rotation(rng, H, 128), synth.gen_rotation(rng, H, 128)
+    ref, rk, rv = O.calibrate_clip(K, V, RK, RV, acc[:, 0], acc[:, 1], GRID, bits, G)
+    o = B.Oscar(B.Config(num_q_heads=Hq, num_kv_heads=H, bits=bits, group_size=G))
+    obj, grk, grv = o.calib_clip(T(K, torch.bfloat16), T(V, torch.bfloat16), T(RK), T(RV), T(acc), GRID)
+    got = obj.cpu().numpy()
+    assert np.all(np.abs(got - ref) <= 1e-3 * np.abs(ref)), np.abs(got - ref).max()
+    for side, (g_pick, o_pick) in enumerate([(grk, rk), (grv, rv)]):
+        tot = np.sort(ref.sum(axis=0)[side])
+        if tot[1] - tot[0] > 1e-2 * tot[0]:      # a clear minimum must be found by both
+            assert g_pick == o_pick, (side, ref.sum(axis=0)[side])
+
+
+def test_calib_clip_planted_outlier_choices():
+    """The provable fixture of the oracle pin (test_oracle_pins.py): channel 0 carries a planted
+    outlier; zero weight on it -> rho < 1, dominant weight -> rho = 1."""
+    import torch
+    from paper_2605_17757_b200 import binding as B
+    rng = np.random.default_rng(6)
+    d, N = 128, 64
+    X = rng.standard_normal((N, 1, d)).astype(np.float32)
+    X[:, 0, 0] = 100.0
+    I = np.eye(d, dtype=np.float32)[None]
+    acc = np.stack([np.eye(d), np.eye(d)])[None].copy()        # [1, 2, d, d]
+    acc[0, 0, 0, 0] = 0.0
+    acc[0, 1, 0, 0] = 1e6
+    o = B.Oscar(B.Config(num_q_heads=1, num_kv_heads=1, bits=2, group_size=64))
+    _, rk, rv = o.calib_clip(T(X, torch.bfloat16), T(X, torch.bfloat16), T(I), T(I), T(acc), [0.98, 1.0])
+    assert rk == 0.98 and rv == 1.0

@@ -483,3 +483,48 @@ def test_attend_mixed_reduces_to_pure_cases():
             ref = [sum(w[t] * float(sv[b, h, t, c]) for t in range(n)) / sum(w) for c in range(0, d, 17)]
             np.testing.assert_allclose(o3[b, i, ::17], ref, atol=1e-12)
             assert abs(l3[b, i] - math.log(sum(w))) < 1e-12
+
+
+# ----------------------------------------------------------------------------------------
+# CalibrateClip (Alg. 1, reading Z34)
+def test_clip_surrogate_equals_explicit_logit_error():
+    """The K surrogate tr(R^T C_Q R E_K) with C_Q = Q^T Q equals the squared logit error
+    sum_{n,j} (q_n k_j^T - q_n khat_j^T)^2 computed from explicit queries (Eq. 1):
+    khat_j = dequant(clip(k_j R)) R^T in the original frame."""
+    rng = np.random.default_rng(5)
+    d, N, Nq = 128, 96, 40
+    Q = rng.standard_normal((Nq, d))
+    K = (rng.standard_normal((N, d)) * np.where(np.arange(d) < 3, 9.0, 1.0)).astype(np.float32)
+    R = np.linalg.qr(rng.standard_normal((d, d)))[0].astype(np.float32)
+    grid = [0.9, 0.96, 1.0]
+    obj = O.clip_objectives(K, R, Q.T @ Q, grid, 2, 64)
+    Kr = O.rotate(K[:, None], R[None])[:, 0]
+    for i, rho in enumerate(grid):
+        c, s16, m16 = O.quantize_rows(O.clip_rows(Kr, rho), 2, 64)
+        Khat = O.dequantize_rows(c, s16, m16, 64) @ R.astype(np.float64).T      # back to the K frame
+        # logits against the rotated-then-unrotated exact keys (R orthogonal in fp64 up to fp32)
+        Kexact = Kr.astype(np.float64) @ R.astype(np.float64).T
+        err = Q @ (Kexact - Khat).T
+        assert abs(obj[i] - (err ** 2).sum()) <= 1e-9 * (err ** 2).sum() + 1e-9
+
+
+def test_calibrate_clip_provable_choices():
+    """Channel 0 carries a planted outlier.  If the covariance target gives channel 0 no
+    weight, clipping it costs nothing and shrinks every other channel's step, so rho < 1
+    must win; if channel 0 dominates the weight, clipping error there dominates and rho = 1
+    must win.  A singleton grid returns its value; equal-magnitude rows tie (first entry)."""
+    rng = np.random.default_rng(6)
+    d, N = 128, 64
+    X = rng.standard_normal((N, 1, d)).astype(np.float32)
+    X[:, 0, 0] = 100.0
+    I = np.eye(d, dtype=np.float32)[None]
+    w0 = np.eye(d)[None].copy(); w0[0, 0, 0] = 0.0              # channel 0 unweighted
+    w1 = np.eye(d)[None].copy(); w1[0, 0, 0] = 1e6              # channel 0 dominant
+    grid = [0.98, 1.0]
+    _, rk, rv = O.calibrate_clip(X, X, I, I, w0, w1, grid, 2, 64)
+    assert rk == 0.98 and rv == 1.0
+    _, rk, rv = O.calibrate_clip(X, X, I, I, w0, w1, [1.0], 2, 64)
+    assert rk == 1.0 and rv == 1.0
+    Y = np.where(rng.random((N, 1, d)) < 0.5, -1.0, 1.0).astype(np.float32)    # |x| all equal
+    obj, rk, rv = O.calibrate_clip(Y, Y, I, I, np.eye(d)[None], np.eye(d)[None], [0.9, 0.96], 2, 64)
+    assert np.allclose(obj[..., 0], obj[..., 1]) and rk == 0.9 and rv == 0.9

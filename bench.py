@@ -293,6 +293,27 @@ def main():
         e3.record()
         torch.cuda.synchronize()
         t_acc, t_ar, t_fin = e0.elapsed_time(e1), e1.elapsed_time(e2), e2.elapsed_time(e3)
+        # on-device S·V for C_S (NEXT-3), one layer: 8 calibration sequences of 8192 tokens
+        Kc = synth.torch_keys(gen, calib_tokens, HKV, D, dev)
+        Vc = synth.torch_values(gen, calib_tokens, HKV, D, dev)
+        starts = torch.arange(0, calib_tokens, 8192, dtype=torch.int32, device=dev)
+        SVd = torch.empty_like(SV)
+        o.calib_sv(Q, Kc, Vc, starts, SVd)
+        es0, es1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        es0.record()
+        o.calib_sv(Q, Kc, Vc, starts, SVd)
+        es1.record()
+        # CalibrateClip (reading Z34) on 8192 rows of that layer, Table 10's 5-point grid
+        RKc, RVc = RK_all[0].contiguous(), RV_all[0].contiguous()
+        ec0, ec1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        o.calib_clip(Kc[:8192], Vc[:8192], RKc, RVc, acc[0], [0.88, 0.92, 0.96, 0.98, 1.0])
+        ec0.record()
+        _, rho_k, rho_v = o.calib_clip(Kc[:8192], Vc[:8192], RKc, RVc, acc[0], [0.88, 0.92, 0.96, 0.98, 1.0])
+        ec1.record()
+        torch.cuda.synchronize()
+        t_sv, t_clip = es0.elapsed_time(es1), ec0.elapsed_time(ec1)
+        sv_flops = 2 * 2 * HQ * D * (calib_tokens // 8192) * (8192 * 8193 // 2)
+        del Kc, Vc, SVd
         sweeps = info.cpu().numpy()
         cov_bytes = NL * 2 * calib_tokens * HQ * D * 2
         cov_flops = NL * 2 * calib_tokens * HQ * 2 * D * D
@@ -303,6 +324,10 @@ def main():
             "accumulate_TFLOPs": cov_flops / t_acc / 1e9,
             "allreduce_ms": t_ar, "allreduce_bytes": acc.numel() * 8,
             "finalize_ms": t_fin, "jacobi_sweeps_max": int(sweeps.max()),
+            "sv_ms_per_layer": t_sv, "sv_TFLOPs": sv_flops / t_sv / 1e9,
+            "sv_config": f"causal S·V, {calib_tokens // 8192} sequences x 8192 tokens, {HQ} q-heads",
+            "clip_ms_per_layer": t_clip, "clip_config": "8192 rows x 8 kv heads x K,V x 5 ratios",
+            "clip_choice_layer0": [rho_k, rho_v],
             "roofline": {"bound": "hbm", "achieved": cov_bytes / t_acc / 1e6, "peak": hbm_peak, "unit": "GB/s",
                          "frac": cov_bytes / t_acc / 1e6 / hbm_peak,
                          "traffic": ncu_traffic(["cov_accum_tc_kernel"]),

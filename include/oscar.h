@@ -62,7 +62,11 @@ typedef struct oscar_ctx oscar_ctx; /* opaque; immutable after create (except os
 typedef struct {
   int32_t head_dim;        /* d; must be a power of two; this build implements d = 128       */
   int32_t num_q_heads;     /* H_q of this rank's shard                                       */
-  int32_t num_kv_heads;    /* H_kv of this shard; H_q % H_kv == 0, g = H_q / H_kv (GQA)       */
+  int32_t num_kv_heads;    /* H_kv of this shard; H_q % H_kv == 0, g = H_q / H_kv (GQA).
+                              Attend implements g <= 8 (OSCAR_ERR_UNSUPPORTED otherwise);
+                              calibration takes any g: a context with H_kv = 1 accumulates one
+                              covariance over all query heads (NEXT-4 shared-rotation mode,
+                              P:L140-144; reading Z14's alternative)                         */
   int32_t bits;            /* b in {2, 3, 4}; b = 3 (codes straddle bytes, reading Z23) runs on
                               the simple CUDA-core kernels, b = 2, 4 also on the tensor-core ones */
   int32_t group_size;      /* G in {32, 64, 128}, G | d; same for K and V (reading Z7)        */
@@ -94,6 +98,16 @@ OSCAR_API size_t oscar_page_bytes(const oscar_ctx* ctx);
  * N = 0 is a no-op; N < 0 or NULL pointers -> OSCAR_ERR_ARG. */
 OSCAR_API oscar_status oscar_calib_accumulate(const oscar_ctx* ctx, const void* Q, const void* SV,
                                     int64_t N, double* acc, void* stream);
+
+/* S·V on the device for the C_S target: SV = softmax(Q Kᵀ·scale + M) V per query
+ * head (Alg. 1), M causal including the diagonal and block-diagonal
+ * across the calibration sequences (reading Z16); query head i attends KV head i/g.  Computed by a
+ * flash-attention forward on the tensor cores (mma.sync bf16, fp32 softmax / accumulation).
+ * Q: bf16 [N][H_q][d]; K, V: bf16 [N][H_kv][d]; seq_starts: device int32 [n_seq], the first
+ * token of each calibration sequence (seq_starts[0] = 0, strictly increasing, < N); SV: bf16
+ * [N][H_q][d] (output; pass it to oscar_calib_accumulate as SV).  N = 0 is a no-op. */
+OSCAR_API oscar_status oscar_calib_sv(const oscar_ctx* ctx, const void* Q, const void* K, const void* V,
+                            const int32_t* seq_starts, int32_t n_seq, int64_t N, void* SV, void* stream);
 
 /* Finalize n_mats (layer, kv-head) pairs: C = acc / n_rows (n_rows = N_total·g), eigen-
  * decompose with a one-CTA parallel cyclic Jacobi in fp64 (λ descending, ties by index,

@@ -24,7 +24,7 @@ EXPORTED = [
     "oscar_create", "oscar_destroy", "oscar_last_error", "oscar_version", "oscar_page_bytes",
     "oscar_calib_accumulate", "oscar_calib_finalize", "oscar_quantize_append",
     "oscar_attend_workspace_bytes", "oscar_attend", "oscar_attend_mixed", "oscar_rotate",
-    "oscar_quantize_rotated", "oscar_set_variant", "oscar_calib_clip",
+    "oscar_quantize_rotated", "oscar_set_variant", "oscar_calib_clip", "oscar_calib_sv",
 ]
 
 
@@ -56,6 +56,7 @@ _sig = {
     "oscar_rotate": (_i32, [_vp, _vp, _vp, _vp, _i64, _vp]),
     "oscar_quantize_rotated": (_i32, [_vp, _vp, _vp, _vp, _i64, _vp, _vp]),
     "oscar_set_variant": (_i32, [_vp, _i32]),
+    "oscar_calib_sv": (_i32, [_vp, _vp, _vp, _vp, _vp, _i32, _i64, _vp, _vp]),
     "oscar_calib_clip": (_i32, [_vp, _vp, _vp, _i64, _vp, _vp, _vp, ctypes.POINTER(ctypes.c_float), _i32, _vp,
                                 _vp]),
 }
@@ -142,6 +143,10 @@ class Oscar:
         _check(_lib.oscar_calib_finalize(self._h, _ptr(acc), n_mats, n_rows, _ptr(R_K), _ptr(R_V),
                                          _ptr(evals), _ptr(info), _stream(stream)),
                "oscar_calib_finalize")
+
+    def calib_sv(self, Q, K, V, seq_starts, SV, stream=None):
+        _check(_lib.oscar_calib_sv(self._h, _ptr(Q), _ptr(K), _ptr(V), _ptr(seq_starts), seq_starts.shape[0],
+                                   Q.shape[0], _ptr(SV), _stream(stream)), "oscar_calib_sv")
 
     def calib_clip(self, K, V, R_K, R_V, acc, grid, obj=None, stream=None):
         """CalibrateClip (reading Z34): surrogate objectives obj [H_kv, 2, n_grid] (fp64, device)

@@ -62,8 +62,8 @@ oscar_status oscar_create(const oscar_config* cfg, oscar_ctx** out) {
   if (c.num_q_heads <= 0 || c.num_kv_heads <= 0 || c.num_q_heads % c.num_kv_heads)
     return fail(OSCAR_ERR_ARG, "need H_q %% H_kv == 0 and both > 0 (got %d, %d)", c.num_q_heads,
                 c.num_kv_heads);
-  const int g = c.num_q_heads / c.num_kv_heads;
-  if (g > 8) return fail(OSCAR_ERR_UNSUPPORTED, "GQA ratio %d > 8 not implemented", g);
+  // any GQA ratio calibrates (num_kv_heads = 1 is NEXT-4's shared-rotation mode); attend
+  // implements g <= 8 and checks it per call
   if (c.bits != 2 && c.bits != 3 && c.bits != 4)
     return fail(OSCAR_ERR_ARG, "bits must be 2, 3 or 4 (got %d)", c.bits);
   if (c.group_size != 32 && c.group_size != 64 && c.group_size != 128)
@@ -79,7 +79,7 @@ oscar_status oscar_create(const oscar_config* cfg, oscar_ctx** out) {
   oscar_ctx* x = new (std::nothrow) oscar_ctx();
   if (!x) return fail(OSCAR_ERR_ARG, "out of host memory");
   x->cfg = c;
-  x->d = c.head_dim; x->hq = c.num_q_heads; x->hkv = c.num_kv_heads; x->g = g;
+  x->d = c.head_dim; x->hq = c.num_q_heads; x->hkv = c.num_kv_heads; x->g = c.num_q_heads / c.num_kv_heads;
   x->bits = c.bits; x->G = c.group_size; x->P = P; x->ng = x->d / x->G;
   x->row_bytes = x->d * x->bits / 8;
   x->vcodes_off = P * x->row_bytes;
@@ -124,6 +124,16 @@ oscar_status oscar_calib_accumulate(const oscar_ctx* ctx, const void* Q, const v
   if (ctx->variant == 0 && oscar::cov_tc_supported(*ctx))
     return cuda_status(oscar::launch_cov_accum_tc(*ctx, Q, SV, N, acc, as_stream(stream)), "cov_accum_tc");
   return cuda_status(oscar::launch_cov_accum(*ctx, Q, SV, N, acc, as_stream(stream)), "cov_accum");
+}
+
+oscar_status oscar_calib_sv(const oscar_ctx* ctx, const void* Q, const void* K, const void* V,
+                            const int32_t* seq_starts, int32_t n_seq, int64_t N, void* SV, void* stream) {
+  if (!ctx) return fail(OSCAR_ERR_ARG, "NULL ctx");
+  if (N < 0 || N > 0x7fffffffLL) return fail(OSCAR_ERR_ARG, "N must be in [0, 2^31) (got %lld)", (long long)N);
+  if (N == 0) return OSCAR_OK;
+  if (n_seq < 1) return fail(OSCAR_ERR_ARG, "n_seq must be >= 1");
+  if (!Q || !K || !V || !seq_starts || !SV) return fail(OSCAR_ERR_ARG, "oscar_calib_sv: NULL pointer");
+  return cuda_status(oscar::launch_calib_sv(*ctx, Q, K, V, seq_starts, n_seq, N, SV, as_stream(stream)), "calib_sv");
 }
 
 oscar_status oscar_calib_clip(const oscar_ctx* ctx, const void* K, const void* V, int64_t N,
@@ -220,6 +230,7 @@ oscar_status oscar_attend(const oscar_ctx* ctx, const void* q, const int32_t* pa
                           void* workspace, size_t workspace_bytes, void* out, int32_t out_fp32,
                           float* lse, void* stream) {
   if (!ctx) return fail(OSCAR_ERR_ARG, "NULL ctx");
+  if (ctx->g > 8) return fail(OSCAR_ERR_UNSUPPORTED, "attend: GQA ratio %d > 8 not implemented", ctx->g);
   if (B < 0 || max_pages < 0) return fail(OSCAR_ERR_ARG, "B and max_pages must be >= 0");
   if (B == 0) return OSCAR_OK;
   if (max_pages == 0) return fail(OSCAR_ERR_ARG, "max_pages must be > 0");
@@ -241,6 +252,7 @@ oscar_status oscar_attend_mixed(const oscar_ctx* ctx, const void* q, const int32
                                 size_t workspace_bytes, void* out, int32_t out_fp32, float* lse,
                                 void* stream) {
   if (!ctx) return fail(OSCAR_ERR_ARG, "NULL ctx");
+  if (ctx->g > 8) return fail(OSCAR_ERR_UNSUPPORTED, "attend: GQA ratio %d > 8 not implemented", ctx->g);
   if (B < 0 || max_pages < 0 || seg_cap < 0) return fail(OSCAR_ERR_ARG, "negative size");
   if (B == 0) return OSCAR_OK;
   if (max_pages == 0) return fail(OSCAR_ERR_ARG, "max_pages must be > 0");

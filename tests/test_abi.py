@@ -59,12 +59,17 @@ def test_create_validation():
            (dict(num_q_heads=30), B.ERR_ARG), (dict(bits=5), B.ERR_ARG),
            (dict(group_size=48), B.ERR_ARG),
            (dict(page_size=20), B.ERR_ARG), (dict(clip_ratio_k=0.0), B.ERR_ARG),
-           (dict(clip_ratio_v=1.5), B.ERR_ARG), (dict(num_q_heads=72, num_kv_heads=8), B.ERR_UNSUPPORTED)]
+           (dict(clip_ratio_v=1.5), B.ERR_ARG)]
     for kw, st in bad:
         with pytest.raises(B.OscarError) as e:
             B.Oscar(B.Config(**kw))
         assert e.value.status == st, kw
     assert "oscar-b200" in B.version()
+    # g > 8 creates (calibration, incl. the shared-rotation mode H_kv = 1) but attend refuses it
+    o = B.Oscar(B.Config(num_q_heads=72, num_kv_heads=8))
+    assert B.raw_call("oscar_attend", o._h, None, None, None, 1, 1, None, None, None, None, 0, None, 0,
+                      None, None) == B.ERR_UNSUPPORTED
+    B.Oscar(B.Config(num_q_heads=32, num_kv_heads=1))
 
 
 def test_page_bytes_matches_format():

@@ -165,6 +165,21 @@ OSCAR_API oscar_status oscar_attend(const oscar_ctx* ctx, const void* q, const i
                           void* workspace, size_t workspace_bytes, void* out, int32_t out_fp32,
                           float* lse, void* stream);
 
+/* One decode step of Alg. 1 `DecodeStep` on the packed cache: QuantizeAndWrite
+ * of the step's new K and V rows (rotate by R_K / R_V, clip, min-max quantize,
+ * pack) at position seq_lens[b] - 1 of sequence b — slot page_table[b][(L-1)/P]·P + (L-1)%P —
+ * then attend(q) over the seq_lens[b] tokens, the new one included (reading Z20).  Same result
+ * as oscar_quantize_append of those rows followed by oscar_attend; one fused prologue kernel
+ * does the appends and the q rotation, and the attention kernel starts streaming the other
+ * pages while it runs.  k_new, v_new: bf16 [B][H_kv][d].  seq_lens[b] = 0 appends nothing and
+ * returns o = 0.  pool is written.  Other arguments as oscar_attend. */
+OSCAR_API oscar_status oscar_decode_step(const oscar_ctx* ctx, const void* q, const void* k_new,
+                               const void* v_new, const int32_t* page_table,
+                               const int32_t* seq_lens, int32_t B, int32_t max_pages, void* pool,
+                               const float* R_K, const float* R_V, void* workspace,
+                               size_t workspace_bytes, void* out, int32_t out_fp32, float* lse,
+                               void* stream);
+
 /* attend over the mixed-precision cache (§4 "KV Cache Layout" P:L537-548: bf16 sink ‖ INT2
  * history ‖ bf16 recent window; Alg. 1 DecodeStep P:L1627-1635): the INT2 history is the first
  * seq_lens[b] tokens of page_table[b] in the pool (as oscar_attend), and the bf16 tokens (sink +

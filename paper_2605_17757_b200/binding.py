@@ -24,7 +24,7 @@ EXPORTED = [
     "oscar_create", "oscar_destroy", "oscar_last_error", "oscar_version", "oscar_page_bytes",
     "oscar_calib_accumulate", "oscar_calib_finalize", "oscar_quantize_append",
     "oscar_attend_workspace_bytes", "oscar_attend", "oscar_attend_mixed", "oscar_rotate",
-    "oscar_quantize_rotated", "oscar_set_variant", "oscar_calib_clip", "oscar_calib_sv",
+    "oscar_quantize_rotated", "oscar_set_variant", "oscar_calib_clip", "oscar_calib_sv", "oscar_decode_step",
 ]
 
 
@@ -51,6 +51,8 @@ _sig = {
     "oscar_attend_workspace_bytes": (_sz, [_vp, _i32, _i32]),
     "oscar_attend": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _vp, _i32,
                             _vp, _vp]),
+    "oscar_decode_step": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _vp,
+                                 _i32, _vp, _vp]),
     "oscar_attend_mixed": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i32,
                                   _vp, _sz, _vp, _i32, _vp, _vp]),
     "oscar_rotate": (_i32, [_vp, _vp, _vp, _vp, _i64, _vp]),
@@ -177,6 +179,17 @@ class Oscar:
                                  page_table.shape[1], _ptr(pool), _ptr(R_K), _ptr(R_V),
                                  _ptr(workspace), workspace.numel() * workspace.element_size(),
                                  _ptr(out), out_fp32, _ptr(lse), _stream(stream)), "oscar_attend")
+
+    def decode_step(self, q, k_new, v_new, page_table, seq_lens, pool, R_K, R_V, workspace, out,
+                    lse=None, stream=None):
+        """Alg. 1 DecodeStep: quantize_append of (k_new, v_new) at position seq_lens[b]-1, then
+        attend(q) over seq_lens[b] tokens (one fused prologue kernel + the attention kernels)."""
+        import torch
+        out_fp32 = 1 if out.dtype == torch.float32 else 0
+        _check(_lib.oscar_decode_step(self._h, _ptr(q), _ptr(k_new), _ptr(v_new), _ptr(page_table),
+                                      _ptr(seq_lens), q.shape[0], page_table.shape[1], _ptr(pool), _ptr(R_K),
+                                      _ptr(R_V), _ptr(workspace), workspace.numel() * workspace.element_size(),
+                                      _ptr(out), out_fp32, _ptr(lse), _stream(stream)), "oscar_decode_step")
 
     def attend_mixed(self, q, page_table, seq_lens, pool, R_K, R_V, seg_k, seg_v, seg_lens, workspace,
                      out, lse=None, stream=None):

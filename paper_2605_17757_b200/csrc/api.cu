@@ -230,7 +230,8 @@ oscar_status oscar_attend(const oscar_ctx* ctx, const void* q, const int32_t* pa
                           void* workspace, size_t workspace_bytes, void* out, int32_t out_fp32,
                           float* lse, void* stream) {
   if (!ctx) return fail(OSCAR_ERR_ARG, "NULL ctx");
-  if (ctx->g > 8) return fail(OSCAR_ERR_UNSUPPORTED, "attend: GQA ratio %d > 8 not implemented", ctx->g);
+  if (ctx->g > 8 || (ctx->g & (ctx->g - 1)))
+    return fail(OSCAR_ERR_UNSUPPORTED, "attend: GQA ratio %d not in {1, 2, 4, 8}", ctx->g);
   if (B < 0 || max_pages < 0) return fail(OSCAR_ERR_ARG, "B and max_pages must be >= 0");
   if (B == 0) return OSCAR_OK;
   if (max_pages == 0) return fail(OSCAR_ERR_ARG, "max_pages must be > 0");
@@ -245,6 +246,28 @@ oscar_status oscar_attend(const oscar_ctx* ctx, const void* q, const int32_t* pa
                      "attend");
 }
 
+oscar_status oscar_decode_step(const oscar_ctx* ctx, const void* q, const void* k_new, const void* v_new,
+                               const int32_t* page_table, const int32_t* seq_lens, int32_t B,
+                               int32_t max_pages, void* pool, const float* R_K, const float* R_V,
+                               void* workspace, size_t workspace_bytes, void* out, int32_t out_fp32,
+                               float* lse, void* stream) {
+  if (!ctx) return fail(OSCAR_ERR_ARG, "NULL ctx");
+  if (ctx->g > 8 || (ctx->g & (ctx->g - 1)))
+    return fail(OSCAR_ERR_UNSUPPORTED, "attend: GQA ratio %d not in {1, 2, 4, 8}", ctx->g);
+  if (B < 0 || max_pages < 0) return fail(OSCAR_ERR_ARG, "B and max_pages must be >= 0");
+  if (B == 0) return OSCAR_OK;
+  if (max_pages == 0) return fail(OSCAR_ERR_ARG, "max_pages must be > 0");
+  if (!q || !k_new || !v_new || !page_table || !seq_lens || !pool || !R_K || !workspace || !out)
+    return fail(OSCAR_ERR_ARG, "oscar_decode_step: NULL pointer");
+  const size_t need = oscar::attend_workspace_bytes(*ctx, B, max_pages);
+  if (workspace_bytes < need)
+    return fail(OSCAR_ERR_ARG, "workspace too small: %zu < %zu", workspace_bytes, need);
+  return cuda_status(oscar::launch_attend(*ctx, q, page_table, seq_lens, B, max_pages, pool, R_K, R_V,
+                                          workspace, out, out_fp32, lse, as_stream(stream), nullptr,
+                                          nullptr, nullptr, 0, k_new, v_new),
+                     "decode_step");
+}
+
 oscar_status oscar_attend_mixed(const oscar_ctx* ctx, const void* q, const int32_t* page_table,
                                 const int32_t* seq_lens, int32_t B, int32_t max_pages, const void* pool,
                                 const float* R_K, const float* R_V, const void* seg_k, const void* seg_v,
@@ -252,7 +275,8 @@ oscar_status oscar_attend_mixed(const oscar_ctx* ctx, const void* q, const int32
                                 size_t workspace_bytes, void* out, int32_t out_fp32, float* lse,
                                 void* stream) {
   if (!ctx) return fail(OSCAR_ERR_ARG, "NULL ctx");
-  if (ctx->g > 8) return fail(OSCAR_ERR_UNSUPPORTED, "attend: GQA ratio %d > 8 not implemented", ctx->g);
+  if (ctx->g > 8 || (ctx->g & (ctx->g - 1)))
+    return fail(OSCAR_ERR_UNSUPPORTED, "attend: GQA ratio %d not in {1, 2, 4, 8}", ctx->g);
   if (B < 0 || max_pages < 0 || seg_cap < 0) return fail(OSCAR_ERR_ARG, "negative size");
   if (B == 0) return OSCAR_OK;
   if (max_pages == 0) return fail(OSCAR_ERR_ARG, "max_pages must be > 0");

@@ -1,13 +1,14 @@
 // attend(q) -> o : decode attention over the packed paged cache (Alg. 1 DecodeStep attention
 // P:L1632-1635, in the rotated frame of the north star; §4 "Decoding Attention Kernel"
 // split-K partial kernel + online-softmax merge kernel).
-//   q_rotate_kernel        q̃ = q · R_K[h] · scale · log2(e)   (fp32, workspace)
+//   attend_prologue_kernel q̃ = q · R_K[h] · scale · log2(e) (+ the decode step's append)
 //   attend_partial_simple  variant 1: CUDA-core reference partial kernel (one CTA per
 //                          (split, kv head, sequence)); the tensor-core kernel is in
 //                          attend_mma.cu (variant 0)
 //   attend_merge_kernel    LSE merge over splits, o = õ · R_Vᵀ, bf16/fp32 store, lse
 #include "common.cuh"
 #include "attend_common.cuh"
+#include "append_epilogue.cuh"
 
 #ifndef OSCAR_PDL_MERGE
 #define OSCAR_PDL_MERGE 1
@@ -15,62 +16,118 @@
 
 namespace oscar {
 
-// ------------------------------------------------------------------ q rotation
-// grid (B, H_kv), 512 threads (16 warps).  Warp w serves query head w mod g of the group and
-// k-slice w / g (16/g slices of 128g/16 input channels): lane l forms the partial dot of columns
-// 4l..4l+3 of q̃ = q · R_K[h] (all its R loads in flight at once); warps 0..g-1 then combine the
-// slices, scale by softmax scale · log2(e) (fp32 q̃ kept for the simple kernel), and emit the
-// 15-bit integer form used by the IMMA QK path: qscale = max|q̃| / 32639, qint = rint(q̃/qscale)
-// (|qint| <= 32639 = 127·256 + 127, so the hi/lo int8 split never overflows), qsum[grp] =
-// Σ_{c in grp} qint; finally all threads write the per-lane IMMA A fragments of the group.
-// PDL: the work depends only on the caller's q and R_K; griddepcontrol.wait at the end keeps
-// "this kernel complete => the preceding kernel complete" for the partial kernel.
-__global__ void __launch_bounds__(512) q_rotate_kernel(const uint16_t* __restrict__ q,
-                                                       const float* __restrict__ RK, int Hq,
-                                                       int g, int lgG, float qscale,
-                                                       float* __restrict__ qt,
-                                                       int16_t* __restrict__ qint,
-                                                       float* __restrict__ qsc,
-                                                       int32_t* __restrict__ qsum,
-                                                       uint32_t* __restrict__ qfrag, int bits,
-                                                       int nt, int32_t* __restrict__ work) {
-  __shared__ __align__(16) float qs[8][kD];
-  __shared__ __align__(16) float ps[16][kD];
-  __shared__ int16_t qis[8][kD];
+// ------------------------------------------------------------------ prologue
+// q rotation (B1), and in decode-step mode also the step's quantize-append (Alg. 1 DecodeStep
+// appends the new row before attending; QuantizeAndWrite P:L1639-1643).
+// grid (B, H_kv), 512 threads (16 warps).  Rows rotated per CTA: the GQ query heads of group h
+// and the new K row by R_K[h], the new V row by R_V[h].  Warp w owns the contraction slice
+// k = 8w .. 8w+7: it loads those 8 rows of R_K (and R_V) once — lane l the float4 of columns
+// 4l..4l+3, 16 loads in flight — and forms partial dots for every row vector; the 16 partials
+// per (row, channel) are summed through smem.  Then:
+//   * warps 0..GQ-1: q̃ = q·R_K·scale·log₂e (fp32, kept for the simple kernel) and the 15-bit
+//     integer form of the IMMA QK path: qscale = max|q̃| / 32639, qint = rint(q̃/qscale)
+//     (|qint| <= 32639 = 127·256 + 127, so the hi/lo int8 split never overflows), qsum[grp] =
+//     Σ_{c in grp} qint; then all threads write the per-lane IMMA A fragments of the group;
+//   * decode step: warp 14 quantizes and stores the K row, warp 15 the V row, at position
+//     seq_lens[b] - 1 of sequence b (the shared clip/min-max/pack epilogue of quantize_append).
+// PDL: launched as an ordinary kernel (every earlier kernel of the stream is complete when it
+// starts) and lets the partial kernel launch at once; the partial kernel's page prefetch only
+// touches pages this kernel does not write (the last page of each sequence waits for
+// griddepcontrol.wait).
+struct PrologueParams {
+  const uint16_t* q;            // [B][H_q][128] bf16
+  const float* RK;              // [H_kv][128][128]
+  const float* RV;              // [H_kv][128][128] or null (pre-rotated V)
+  int Hq, lgG, bits, nt;
+  float qscale;                 // softmax scale · log2(e)
+  float* qt;
+  int16_t* qint;
+  float* qsc;
+  int32_t* qsum;
+  uint32_t* qfrag;              // null: simple kernel path
+  int32_t* work;                // null: simple kernel path
+  // decode step (null knew: plain attend)
+  const uint16_t* knew;         // [B][H_kv][128] bf16
+  const uint16_t* vnew;
+  const int32_t* page_table;
+  const int32_t* seq_lens;
+  int max_pages;
+  uint8_t* pool;
+  EpiParams ep;
+};
+
+template <int GQ>
+__global__ void __launch_bounds__(512) attend_prologue_kernel(PrologueParams pp) {
+  constexpr int NR = GQ + 2;                         // q heads, K row, V row
+  extern __shared__ __align__(16) float psm[];
+  float* ps = psm;                                   // [16][NR][128] partial dots
+  __shared__ __align__(16) float xs[NR][kD];         // input rows (fp32)
+  __shared__ __align__(16) float ys[NR][kD];         // rotated rows
+  __shared__ int16_t qis[GQ][kD];
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   const int b = blockIdx.x, h = blockIdx.y, tid = threadIdx.x;
   const int w = tid >> 5, lane = tid & 31;
-  const int G = 1 << lgG;
-  if (work && b == 0 && h == 0 && tid == 0) *work = 0;   // reset the work-item counter
-  for (int e = tid; e < g * (kD / 4); e += 512) {
-    const int hd = e >> 5, l4 = e & 31;
-    const uint2 u = reinterpret_cast<const uint2*>(q + ((size_t)b * Hq + (size_t)h * g + hd) * kD)[l4];
-    reinterpret_cast<float4*>(qs[hd])[l4] =
-        make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xffff0000u),
-                    __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xffff0000u));
+  const int G = 1 << pp.lgG;
+  const bool dec = pp.knew != nullptr;
+  if (pp.work && b == 0 && h == 0 && tid == 0) *pp.work = 0;   // reset the work-item counter
+  for (int e = tid; e < NR * (kD / 4); e += 512) {
+    const int r = e >> 5, l4 = e & 31;
+    const uint16_t* src = r < GQ ? pp.q + ((size_t)b * pp.Hq + (size_t)h * GQ + r) * kD
+                        : (dec ? (r == GQ ? pp.knew : pp.vnew) + ((size_t)b * gridDim.y + h) * kD : nullptr);
+    float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (src) {
+      const uint2 u = reinterpret_cast<const uint2*>(src)[l4];
+      f = make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xffff0000u),
+                      __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xffff0000u));
+    }
+    reinterpret_cast<float4*>(xs[r])[l4] = f;
   }
   __syncthreads();
   {
-    const int hd = w % g, ks = w / g, kn = (kD * g) / 16;
-    const float4* R4 = reinterpret_cast<const float4*>(RK + (size_t)h * kD * kD + (size_t)ks * kn * kD) + lane;
-    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-#pragma unroll 32
-    for (int k = 0; k < kn; ++k) {
-      const float4 r = R4[(size_t)k * (kD / 4)];
-      const float x = qs[hd][ks * kn + k];
-      a0 = fmaf(x, r.x, a0); a1 = fmaf(x, r.y, a1); a2 = fmaf(x, r.z, a2); a3 = fmaf(x, r.w, a3);
+    const float4* RK4 = reinterpret_cast<const float4*>(pp.RK + (size_t)h * kD * kD) + (size_t)8 * w * 32 + lane;
+    const bool rv = dec && pp.RV;
+    const float4* RV4 = rv ? reinterpret_cast<const float4*>(pp.RV + (size_t)h * kD * kD) + (size_t)8 * w * 32 + lane
+                           : nullptr;
+    float4 rk[8], rvv[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) rk[i] = __ldg(RK4 + i * 32);
+    if (rv) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) rvv[i] = __ldg(RV4 + i * 32);
     }
-    reinterpret_cast<float4*>(ps[w])[lane] = make_float4(a0, a1, a2, a3);
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      if (r > GQ && !rv) break;
+      if (r == GQ && !dec) break;
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float x = xs[r][8 * w + i];
+        const float4 m = r <= GQ ? rk[i] : rvv[i];
+        a.x = fmaf(x, m.x, a.x); a.y = fmaf(x, m.y, a.y); a.z = fmaf(x, m.z, a.z); a.w = fmaf(x, m.w, a.w);
+      }
+      reinterpret_cast<float4*>(ps + ((size_t)w * NR + r) * kD)[lane] = a;
+    }
   }
   __syncthreads();
-  if (w < g) {
-    const size_t row = (size_t)b * Hq + (size_t)h * g + w;
-    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int ks = 0; ks < 16 / g; ++ks) {
-      const float4 x = reinterpret_cast<const float4*>(ps[ks * g + w])[lane];
-      a.x += x.x; a.y += x.y; a.z += x.z; a.w += x.w;
+  for (int e = tid; e < NR * kD; e += 512) {
+    const int r = e >> 7, c = e & (kD - 1);
+    float y;
+    if (r == GQ + 1 && !pp.RV) {
+      y = xs[r][c];                                  // pre-rotated V (NEXT-2): identity
+    } else {
+      y = 0.f;
+#pragma unroll
+      for (int ww = 0; ww < 16; ++ww) y += ps[((size_t)ww * NR + r) * kD + c];
     }
-    a.x *= qscale; a.y *= qscale; a.z *= qscale; a.w *= qscale;
-    reinterpret_cast<float4*>(qt + row * kD)[lane] = a;
+    ys[r][c] = y;
+  }
+  __syncthreads();
+  if (w < GQ) {
+    const size_t row = (size_t)b * pp.Hq + (size_t)h * GQ + w;
+    float4 a = reinterpret_cast<const float4*>(ys[w])[lane];
+    a.x *= pp.qscale; a.y *= pp.qscale; a.z *= pp.qscale; a.w *= pp.qscale;
+    reinterpret_cast<float4*>(pp.qt + row * kD)[lane] = a;
     float mx = fmaxf(fmaxf(fabsf(a.x), fabsf(a.y)), fmaxf(fabsf(a.z), fabsf(a.w)));
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     const float s = mx > 0.f ? mx / 32639.f : 1.f;
@@ -80,31 +137,41 @@ __global__ void __launch_bounds__(512) q_rotate_kernel(const uint16_t* __restric
     const int v3 = max(-32639, min(32639, __float2int_rn(a.w / s)));
     const uint2 pk = make_uint2((uint32_t)(v0 & 0xffff) | ((uint32_t)v1 << 16),
                                 (uint32_t)(v2 & 0xffff) | ((uint32_t)v3 << 16));
-    reinterpret_cast<uint2*>(qint + row * kD)[lane] = pk;
+    reinterpret_cast<uint2*>(pp.qint + row * kD)[lane] = pk;
     reinterpret_cast<uint2*>(qis[w])[lane] = pk;
-    if (lane == 0) qsc[row] = s;
+    if (lane == 0) pp.qsc[row] = s;
     int gs = v0 + v1 + v2 + v3;                    // lanes of one group: G/4 consecutive lanes
     for (int o = 1; o < (G >> 2); o <<= 1) gs += __shfl_xor_sync(0xffffffffu, gs, o);
-    if ((lane & ((G >> 2) - 1)) == 0) qsum[row * 8 + (lane * 4 >> lgG)] = gs;
+    if ((lane & ((G >> 2) - 1)) == 0) pp.qsum[row * 8 + (lane * 4 >> pp.lgG)] = gs;
+  } else if (dec && w >= 14) {
+    const int isV = w - 14;
+    const int L = pp.seq_lens[b];
+    if (L > 0) {
+      const int pos = L - 1;
+      const int64_t slot = (int64_t)pp.page_table[(size_t)b * pp.max_pages + pos / pp.ep.P] * pp.ep.P + pos % pp.ep.P;
+      const float4 y4 = reinterpret_cast<const float4*>(ys[GQ + isV])[lane];
+      float y[4] = {y4.x, y4.y, y4.z, y4.w};
+      quantize_store_row_warp(pp.ep, y, lane, slot, h, isV, pp.pool);
+    }
   }
   __syncthreads();
   // IMMA A fragments for attend_partial_mma: word (j, kk, r) of lane (gid, t) holds the
   // hi (r even) / lo (r odd) int8 of qint[head][channel] for combo 8j + gid = grp·g + head,
   // zero outside the combo's group (see attend_mma.cu)
-  if (qfrag) {
-    const int nc = g << (7 - lgG);
-    uint32_t* dst = qfrag + ((size_t)b * gridDim.y + h) * nt * 16 * 32;
-    for (int wd = tid; wd < nt * 16 * 32; wd += 512) {
+  if (pp.qfrag) {
+    const int nc = GQ << (7 - pp.lgG);
+    uint32_t* dst = pp.qfrag + ((size_t)b * gridDim.y + h) * pp.nt * 16 * 32;
+    for (int wd = tid; wd < pp.nt * 16 * 32; wd += 512) {
       const int ln = wd & 31, rest = wd >> 5;
       const int r = rest & 3, kk = (rest >> 2) & 3, j = rest >> 4;
       const int gid = ln >> 2, t = ln & 3, cb = 8 * j + gid;
       uint32_t v = 0;
       if (cb < nc) {
-        const int grp = cb / g, hd = cb - grp * g;
+        const int grp = cb / GQ, hd = cb - grp * GQ;
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
-          const int ch = qk_channel(bits, kk, 4 * t + m + ((r & 2) ? 16 : 0));
-          if ((ch >> lgG) != grp) continue;
+          const int ch = qk_channel(pp.bits, kk, 4 * t + m + ((r & 2) ? 16 : 0));
+          if ((ch >> pp.lgG) != grp) continue;
           const int qv = qis[hd][ch];
           const int hi8 = (qv + 128) >> 8;
           const int val = (r & 1) ? (qv - 256 * hi8) : hi8;
@@ -114,7 +181,6 @@ __global__ void __launch_bounds__(512) q_rotate_kernel(const uint16_t* __restric
       dst[wd] = v;
     }
   }
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");
 }
 
 // ------------------------------------------------------------------ simple partial kernel
@@ -432,7 +498,7 @@ cudaError_t launch_attend(const oscar_ctx& c, const void* q, const int32_t* page
                           const int32_t* seq_lens, int B, int max_pages, const void* pool,
                           const float* RK, const float* RV, void* ws, void* out, int out_fp32,
                           float* lse, cudaStream_t s, const void* seg_k, const void* seg_v,
-                          const int32_t* seg_lens, int seg_cap) {
+                          const int32_t* seg_lens, int seg_cap, const void* k_new, const void* v_new) {
   const bool mma = c.variant == 0 && attend_mma_supported(c);
   AttnParams p{};
   p.hq = c.hq; p.hkv = c.hkv; p.g = c.g; p.P = c.P; p.bits = c.bits; p.G = c.G; p.ng = c.ng;
@@ -469,18 +535,27 @@ cudaError_t launch_attend(const oscar_ctx& c, const void* q, const int32_t* page
   while ((1 << lgG) < c.G) ++lgG;
   cudaError_t e = cudaSuccess;
   {
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(B, c.hkv);
-    cfg.blockDim = dim3(512);
-    cfg.dynamicSmemBytes = 0;
-    cfg.stream = s;
-    cfg.attrs = pdl;
-    cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, q_rotate_kernel, static_cast<const uint16_t*>(q), RK, c.hq, c.g, lgG,
-                           c.scale * kLog2e, p.qt, p.qint, p.qscale, p.qsum, mma ? p.qfrag : nullptr, c.bits,
-                           p.nt, mma ? p.work : nullptr);
+    PrologueParams pp{};
+    pp.q = static_cast<const uint16_t*>(q); pp.RK = RK; pp.RV = RV;
+    pp.Hq = c.hq; pp.lgG = lgG; pp.bits = c.bits; pp.nt = p.nt; pp.qscale = c.scale * kLog2e;
+    pp.qt = p.qt; pp.qint = p.qint; pp.qsc = p.qscale; pp.qsum = p.qsum;
+    pp.qfrag = mma ? p.qfrag : nullptr; pp.work = mma ? p.work : nullptr;
+    pp.knew = static_cast<const uint16_t*>(k_new); pp.vnew = static_cast<const uint16_t*>(v_new);
+    pp.page_table = page_table; pp.seq_lens = seq_lens; pp.max_pages = max_pages;
+    pp.pool = static_cast<uint8_t*>(const_cast<void*>(pool));
+    pp.ep = make_epi_params(c);
+    void (*fn)(PrologueParams) = c.g == 1 ? attend_prologue_kernel<1> : c.g == 2 ? attend_prologue_kernel<2>
+                               : c.g == 4 ? attend_prologue_kernel<4> : attend_prologue_kernel<8>;
+    const int psmem = 16 * (c.g + 2) * kD * (int)sizeof(float);
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, psmem);
+    if (e != cudaSuccess) return e;
+    // an ordinary launch (not PDL): every earlier kernel of the stream has completed when it
+    // starts, so the partial kernel's early page prefetch never races the caller's writes
+    fn<<<dim3(B, c.hkv), 512, psmem, s>>>(pp);
+    e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
+  p.protect_last = k_new != nullptr;
   if (!mma) {
     const int smem = (8 * kD + 64 + 8 * c.P + 24) * 4 + c.page_bytes;
     e = cudaFuncSetAttribute(attend_partial_simple, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

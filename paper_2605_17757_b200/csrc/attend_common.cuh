@@ -26,6 +26,8 @@ struct AttnParams {
   float* seg_o;                // [B][H_q][128] unnormalized Σ p v (null: no segment)
   float* seg_m;                // [B][H_q]
   float* seg_l;                // [B][H_q]
+  int protect_last;            // decode step: the prologue writes each sequence's last page, so
+                               // the partial kernel loads it only after griddepcontrol.wait
 };
 
 bool attend_mma_supported(const oscar_ctx& c);

@@ -45,7 +45,8 @@ cudaError_t launch_attend(const oscar_ctx& c, const void* q, const int32_t* page
                           const int32_t* seq_lens, int B, int max_pages, const void* pool,
                           const float* RK, const float* RV, void* ws, void* out, int out_fp32,
                           float* lse, cudaStream_t s, const void* seg_k, const void* seg_v,
-                          const int32_t* seg_lens, int seg_cap);
+                          const int32_t* seg_lens, int seg_cap, const void* k_new = nullptr,
+                          const void* v_new = nullptr);
 
 // ---------------------------------------------------------------- device helpers
 __device__ __forceinline__ float bf16_to_f32(uint16_t b) {

@@ -1,0 +1,117 @@
+"""GPU parity of oscar_decode_step — one Alg. 1 DecodeStep: QuantizeAndWrite of
+the step's new K/V row at position seq_lens[b]-1, then attention over the
+seq_lens[b] tokens including it (reading Z20).  The oracle runs the same two steps with its own
+quantize_append and attend on the same seeded inputs.  Bars as test_gpu_parity.py: pool bytes
+equal except rounding-boundary flips of the fp32 rotation, outputs within 2e-3 max-abs (fp32
+output mode), lse within the IMMA path's 15-bit q̃ bound."""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2605_17757_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def T(x, dtype=None):
+    import torch
+    t = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    return t.to(dtype) if dtype is not None else t
+
+
+def make(**kw):
+    from paper_2605_17757_b200 import binding as B
+    return B.Oscar(B.Config(**kw))
+
+
+@pytest.mark.parametrize("cfg", [
+    dict(name="C2small", Hq=32, Hkv=8, bits=2, G=64, L=[1000, 65, 1, 64, 129]),   # new page, 1-token seq
+    dict(name="g8", Hq=16, Hkv=2, bits=2, G=64, L=[700, 130]),
+    dict(name="b4G32", Hq=8, Hkv=2, bits=4, G=32, L=[450, 64]),
+    dict(name="g1", Hq=2, Hkv=2, bits=2, G=128, L=[300]),
+    dict(name="b3", Hq=8, Hkv=2, bits=3, G=64, L=[333, 2]),                        # simple kernels
+    dict(name="empty", Hq=8, Hkv=2, bits=2, G=64, L=[200, 0]),                     # seq_len 0: no append
+])
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("prerot_v", [False, True])
+def test_decode_step_parity(cfg, variant, prerot_v):
+    import torch
+    rng = np.random.default_rng(abs(hash((cfg["name"], variant, prerot_v))) % 2 ** 31)
+    Hq, Hkv, L = cfg["Hq"], cfg["Hkv"], cfg["L"]
+    B = len(L)
+    fmt = O.PageFormat(128, cfg["bits"], cfg["G"], 64)
+    max_pages = max(1, (max(L) + 63) // 64)
+    pt = synth.contiguous_page_table(B, max_pages, shuffle_rng=rng)
+    RK = synth.gen_rotation(rng, Hkv, 128)
+    RV = np.broadcast_to(np.eye(128, dtype=np.float32), (Hkv, 128, 128)).copy() if prerot_v \
+        else synth.gen_rotation(rng, Hkv, 128)
+    pool = np.zeros((B * max_pages, Hkv, fmt.page_bytes), np.uint8)
+    for b in range(B):                       # history: the first L-1 tokens, written by the oracle
+        n = max(L[b] - 1, 0)
+        if n:
+            slots = synth.slots_for(pt[b:b + 1], np.arange(n)[None], 64).reshape(-1)
+            O.quantize_append(synth.gen_keys(rng, n, Hkv, 128), synth.gen_values(rng, n, Hkv, 128), slots,
+                              RK, RV, fmt, pool)
+    k_new = synth.gen_keys(rng, B, Hkv, 128)
+    v_new = synth.gen_values(rng, B, Hkv, 128)
+    q = synth.gen_decode_q(rng, B, Hq, 128)
+    # oracle: QuantizeAndWrite at position L-1, then attend over L tokens
+    ref_pool = pool.copy()
+    live = [b for b in range(B) if L[b] > 0]
+    new_slots = np.array([pt[b, (L[b] - 1) // 64] * 64 + (L[b] - 1) % 64 for b in live], np.int64)
+    O.quantize_append(k_new[live], v_new[live], new_slots, RK, RV, fmt, ref_pool)
+    ref, ref_lse = O.attend(q, pt, L, ref_pool, RK, RV, fmt, Hkv)
+
+    o = make(num_q_heads=Hq, num_kv_heads=Hkv, bits=cfg["bits"], group_size=cfg["G"])
+    o.set_variant(variant)
+    gpool = T(pool)
+    ws = torch.empty(o.attend_workspace_bytes(B, max_pages), dtype=torch.uint8, device="cuda")
+    out = torch.empty((B, Hq, 128), dtype=torch.float32, device="cuda")
+    lse = torch.empty((B, Hq), dtype=torch.float32, device="cuda")
+    o.decode_step(T(q, torch.bfloat16), T(k_new, torch.bfloat16), T(v_new, torch.bfloat16), T(pt),
+                  T(np.asarray(L, np.int32)), gpool, T(RK), None if prerot_v else T(RV), ws, out, lse)
+    torch.cuda.synchronize()
+    got_pool = gpool.cpu().numpy()
+    assert (got_pool != ref_pool).sum() <= 4 * max(1, len(live)), "pool differs beyond rounding flips"
+    assert np.abs(out.cpu().numpy() - ref).max() <= 2e-3
+    lg = lse.cpu().numpy()
+    fin = np.isfinite(ref_lse)
+    assert np.array_equal(np.isfinite(lg), fin)
+    assert (np.abs(lg[fin] - ref_lse[fin]) <= 1e-3 + 1e-4 * np.abs(ref_lse[fin])).all()
+
+
+def test_decode_step_equals_append_then_attend():
+    """The fused call and the two-call sequence (quantize_append, then attend) agree: identical
+    outputs wherever the two paths' fp32 rotations round the new row's codes the same way."""
+    import torch
+    rng = np.random.default_rng(11)
+    Hq, Hkv, B, L = 32, 8, 4, [640, 1000, 64, 65]
+    fmt = O.PageFormat(128, 2, 64, 64)
+    max_pages = (max(L) + 63) // 64
+    pt = synth.contiguous_page_table(B, max_pages, shuffle_rng=rng)
+    RK, RV = synth.gen_rotation(rng, Hkv, 128), synth.gen_rotation(rng, Hkv, 128)
+    pool = np.zeros((B * max_pages, Hkv, fmt.page_bytes), np.uint8)
+    for b in range(B):
+        n = L[b] - 1
+        slots = synth.slots_for(pt[b:b + 1], np.arange(n)[None], 64).reshape(-1)
+        O.quantize_append(synth.gen_keys(rng, n, Hkv, 128), synth.gen_values(rng, n, Hkv, 128), slots, RK, RV,
+                          fmt, pool)
+    k_new, v_new = synth.gen_keys(rng, B, Hkv, 128), synth.gen_values(rng, B, Hkv, 128)
+    q = synth.gen_decode_q(rng, B, Hq, 128)
+    o = make(num_q_heads=Hq, num_kv_heads=Hkv)
+    ws = torch.empty(o.attend_workspace_bytes(B, max_pages), dtype=torch.uint8, device="cuda")
+    args = (T(pt), T(np.asarray(L, np.int32)))
+    p1, p2 = T(pool), T(pool)
+    o1 = torch.empty((B, Hq, 128), dtype=torch.float32, device="cuda")
+    o2 = torch.empty_like(o1)
+    o.decode_step(T(q, torch.bfloat16), T(k_new, torch.bfloat16), T(v_new, torch.bfloat16), *args, p1, T(RK),
+                  T(RV), ws, o1)
+    slots = T(np.array([pt[b, (L[b] - 1) // 64] * 64 + (L[b] - 1) % 64 for b in range(B)], np.int64))
+    o.quantize_append(T(k_new, torch.bfloat16), T(v_new, torch.bfloat16), slots, T(RK), T(RV), p2)
+    o.attend(T(q, torch.bfloat16), *args, p2, T(RK), T(RV), ws, o2)
+    torch.cuda.synchronize()
+    if torch.equal(p1, p2):
+        assert torch.equal(o1, o2)
+    else:
+        assert (p1 != p2).sum().item() <= 4 * B
+        assert (o1 - o2).abs().max().item() <= 2e-3

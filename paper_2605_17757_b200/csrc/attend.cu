@@ -45,6 +45,7 @@ struct PrologueParams {
   float* qsc;
   int32_t* qsum;
   uint32_t* qfrag;              // null: simple kernel path
+  int tq;                       // 1: fragments for the token-row QK layout of attend_partial_mma
   int32_t* work;                // null: simple kernel path
   // decode step (null knew: plain attend)
   const uint16_t* knew;         // [B][H_kv][128] bf16
@@ -158,7 +159,32 @@ __global__ void __launch_bounds__(512) attend_prologue_kernel(PrologueParams pp)
   // IMMA A fragments for attend_partial_mma: word (j, kk, r) of lane (gid, t) holds the
   // hi (r even) / lo (r odd) int8 of qint[head][channel] for combo 8j + gid = grp·g + head,
   // zero outside the combo's group (see attend_mma.cu)
-  if (pp.qfrag) {
+  if (pp.qfrag && pp.tq) {
+    // token-row QK layout (attend_mma.cu, TQ): B-fragment word (jt, kk, r) of lane (gid, t)
+    // holds, for column gid = (head 4·jt + gid/2, hi|lo = gid&1), the int8 of qint at the
+    // k-slots 4t + i + 16r (i = 0..3) <-> channel 16·j + 4·i + 2(kk&1) + r, j = t or 4 + t
+    // for kk < 2 or >= 2
+    constexpr int NTQ = (GQ + 3) / 4;
+    uint32_t* dst = pp.qfrag + ((size_t)b * gridDim.y + h) * NTQ * 8 * 32;
+    for (int wd = tid; wd < NTQ * 8 * 32; wd += 512) {
+      const int ln = wd & 31, rest = wd >> 5;
+      const int r = rest & 1, kk = (rest >> 1) & 3, jt = rest >> 3;
+      const int gid = ln >> 2, t = ln & 3;
+      const int hd = 4 * jt + (gid >> 1), lo = gid & 1;
+      uint32_t v = 0;
+      if (hd < GQ) {
+        const int j = (kk >> 1) ? 4 + t : t, sft = 2 * (kk & 1) + r;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int qv = qis[hd][16 * j + 4 * i + sft];
+          const int hi8 = (qv + 128) >> 8;
+          const int val = lo ? (qv - 256 * hi8) : hi8;
+          v |= (uint32_t)(val & 0xff) << (8 * i);
+        }
+      }
+      dst[wd] = v;
+    }
+  } else if (pp.qfrag) {
     const int nc = GQ << (7 - pp.lgG);
     uint32_t* dst = pp.qfrag + ((size_t)b * gridDim.y + h) * pp.nt * 16 * 32;
     for (int wd = tid; wd < pp.nt * 16 * 32; wd += 512) {
@@ -299,91 +325,158 @@ __global__ void __launch_bounds__(128) attend_partial_simple(AttnParams p) {
 }
 
 // ------------------------------------------------------------------ merge
-// grid (B·H_q), 512 threads (16 warps): one CTA per (sequence, query head) row, so the whole
-// machine works on the 16 MB of partials at once.  All threads read the split maxima (block max
-// M, weights w_s = 2^(m_s - M), Σ w_s l_s); warp w sums splits s ≡ w (mod 16) with lane = 4
-// channels; threads < 128 add the 16 warp partials; then warp w computes output rows
-// c' ≡ w (mod 16) of o = õ · R_V[h]ᵀ (coalesced 512-B rows of R_V, shuffle reduction) and adds
-// the original-frame bf16 segment part (NEXT-1).  PDL: griddepcontrol.wait guards the partials.
-__global__ void __launch_bounds__(512) attend_merge_kernel(AttnParams p, const float* __restrict__ RV,
+// LSE merge of the split-K partials + un-rotation o = õ·R_Vᵀ (reading Z21).
+// grid (B, H_kv), 256 threads (8 warps): one CTA per (sequence, KV head), so the g query heads
+// of the group share one copy of R_V[h].  Before griddepcontrol.wait (it only touches the
+// caller's inputs) R_V[h] (64 KB) is bulk-copied into smem.  Then warp w serves head w mod g,
+// splits s ≡ w / g (mod 8/g): each lane issues all loads of a batch of up to 16 splits at once
+// (partial row float4 = channels 4l..4l+3, split max and sum) and folds them with a running max;
+// the 8/g warps of a head and the NEXT-1 segment are combined through smem.  Un-rotation:
+// thread (c', half) forms output channel c' of every other head from smem, the contraction index
+// rotated by lane (c = 4·((k + lane) mod 32)) so the 32 rows of a warp hit distinct banks.
+namespace {
+__device__ __forceinline__ uint32_t msmem_u32(const void* ptr) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(ptr));
+}
+}  // namespace
+
+template <int GQ>
+__global__ void __launch_bounds__(256) attend_merge_kernel(AttnParams p, const float* __restrict__ RV,
                                                            void* __restrict__ out, int out_fp32,
                                                            float* __restrict__ lse) {
-  extern __shared__ float wsp[];                     // [n_splits] weights
-  __shared__ __align__(16) float po[16][kD];
-  __shared__ __align__(16) float ot[kD];
-  __shared__ float red[16];
-  __shared__ float bc[3];                            // M, 1/L, w_seg/L
-  const int row = blockIdx.x, tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
-  const int h = (row % p.hq) / p.g;
+  constexpr int WPH = 8 / GQ;                        // warps per query head
+  constexpr int NB = 16;                             // splits per load batch per warp
+  constexpr int HPT = (GQ + 1) / 2;                  // heads per thread in the un-rotation
+  extern __shared__ __align__(128) float Rs[];       // [128][128] R_V[h]
+  __shared__ __align__(16) float po[8][kD];
+  __shared__ __align__(16) float ot[GQ][kD];
+  __shared__ float pm[8], pl[8], sws[GQ];
+  __shared__ __align__(8) uint64_t bar;
+  const int b = blockIdx.x, h = blockIdx.y, tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  if (RV && tid == 0) {
+    const uint32_t bb = msmem_u32(&bar);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bb));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bb), "r"(kD * kD * 4) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     msmem_u32(Rs)),
+                 "l"(RV + (size_t)h * kD * kD), "r"(kD * kD * 4), "r"(bb)
+                 : "memory");
+  }
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
+#ifdef OSCAR_MERGE_EMPTY   // A/B builds only: launch + dependency cost of the merge
+  if (RV) {
+    asm volatile("{\n.reg .pred P1;\nWAIT_E%=:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n@!P1 bra WAIT_E%=;\n}\n" ::"r"(msmem_u32(&bar)) : "memory");
+  }
+  return;
+#endif
   const int ns = p.n_splits;
-  const size_t row0 = (size_t)row * ns;
-  const bool seg = p.seg_o != nullptr;
-  float M = seg ? p.seg_m[row] : -INFINITY;
-  for (int s = tid; s < ns; s += 512) M = fmaxf(M, p.ws_m[row0 + s]);
-  for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-  if (lane == 0) red[w] = M;
-  __syncthreads();
-  M = red[0];
-#pragma unroll
-  for (int i = 1; i < 16; ++i) M = fmaxf(M, red[i]);
-  __syncthreads();
-  float L = 0.f;
-  for (int s = tid; s < ns; s += 512) {
-    const float wt = M == -INFINITY ? 0.f : exp2f(p.ws_m[row0 + s] - M);   // 0 for empty splits
-    wsp[s] = wt;
-    L = fmaf(p.ws_l[row0 + s], wt, L);
-  }
-  for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
-  if (lane == 0) red[w] = L;
-  __syncthreads();
-  if (tid == 0) {
-    float Ls = 0.f;
-    for (int i = 0; i < 16; ++i) Ls += red[i];
-    const float wseg = (seg && M != -INFINITY) ? exp2f(p.seg_m[row] - M) : 0.f;
-    if (seg) Ls += p.seg_l[row] * wseg;
-    const float inv = Ls > 0.f ? 1.f / Ls : 0.f;
-    bc[0] = M; bc[1] = inv; bc[2] = wseg * inv;
-    if (lse) lse[row] = (Ls > 0.f) ? (M + log2f(Ls)) * 0.6931471805599453f : -INFINITY;
-  }
   {
-    float4 o4 = make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4* pov = reinterpret_cast<const float4*>(p.ws_o + row0 * kD) + lane;
-#pragma unroll 4
-    for (int s = w; s < ns; s += 16) {
-      const float wt = wsp[s];
-      const float4 x = pov[(size_t)s * (kD / 4)];
-      o4.x = fmaf(x.x, wt, o4.x); o4.y = fmaf(x.y, wt, o4.y);
-      o4.z = fmaf(x.z, wt, o4.z); o4.w = fmaf(x.w, wt, o4.w);
-    }
-    reinterpret_cast<float4*>(po[w])[lane] = o4;
-  }
-  __syncthreads();
-  if (tid < kD) {
-    float o = 0.f;
+    const int hd = w % GQ, part = w / GQ;
+    const size_t rbh = (size_t)b * p.hq + (size_t)h * GQ + hd;
+    auto prow = [&](int s) -> size_t { return rbh * ns + s; };
+    float mw = -INFINITY, Lw = 0.f;
+    float4 ow = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s0 = part; s0 < ns; s0 += WPH * NB) {
+      float4 x[NB];
+      float ms[NB], ls[NB];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) o += po[i][tid];
-    ot[tid] = o * bc[1];
+      for (int k = 0; k < NB; ++k) {
+        const int s = s0 + k * WPH;
+        const bool ok = s < ns;
+        const size_t r = ok ? prow(s) : 0;
+        x[k] = ok ? __ldcg(reinterpret_cast<const float4*>(p.ws_o + r * kD) + lane)
+                  : make_float4(0.f, 0.f, 0.f, 0.f);
+        ms[k] = ok ? __ldcg(p.ws_m + r) : -INFINITY;
+        ls[k] = ok ? __ldcg(p.ws_l + r) : 0.f;
+      }
+      float nm = mw;
+#pragma unroll
+      for (int k = 0; k < NB; ++k) nm = fmaxf(nm, ms[k]);
+      const float alpha = mw == nm ? 1.f : exp2f(mw - nm);      // 0 from -inf
+      ow.x *= alpha; ow.y *= alpha; ow.z *= alpha; ow.w *= alpha;
+      Lw *= alpha;
+#pragma unroll
+      for (int k = 0; k < NB; ++k) {
+        const float wt = ms[k] == -INFINITY ? 0.f : exp2f(ms[k] - nm);   // 0 for empty splits
+        if (ms[k] == -INFINITY) {                  // (their õ and l are never written)
+          x[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+          ls[k] = 0.f;
+        }
+        ow.x = fmaf(x[k].x, wt, ow.x); ow.y = fmaf(x[k].y, wt, ow.y);
+        ow.z = fmaf(x[k].z, wt, ow.z); ow.w = fmaf(x[k].w, wt, ow.w);
+        Lw = fmaf(ls[k], wt, Lw);
+      }
+      mw = nm;
+    }
+    reinterpret_cast<float4*>(po[w])[lane] = ow;
+    if (lane == 0) { pm[w] = mw; pl[w] = Lw; }
   }
   __syncthreads();
-  const float4 o4 = reinterpret_cast<const float4*>(ot)[lane];
-  const float sw = bc[2];
-#pragma unroll 4
-  for (int cp = w; cp < kD; cp += 16) {
-    float v;
-    if (RV) {
-      const float4 r4 = reinterpret_cast<const float4*>(RV + (size_t)h * kD * kD + (size_t)cp * kD)[lane];
-      v = r4.x * o4.x + r4.y * o4.y + r4.z * o4.z + r4.w * o4.w;
-      for (int of = 16; of > 0; of >>= 1) v += __shfl_xor_sync(0xffffffffu, v, of);
-    } else {
-      v = ot[cp];                       // pre-rotated V (NEXT-2): õ is already in V's frame
+  const bool seg = p.seg_o != nullptr;
+  for (int e = tid; e < GQ * kD; e += 256) {
+    const int hd = e >> 7, c = e & (kD - 1);
+    const size_t row = (size_t)b * p.hq + (size_t)h * GQ + hd;
+    float M = seg ? p.seg_m[row] : -INFINITY;
+#pragma unroll
+    for (int j = 0; j < WPH; ++j) M = fmaxf(M, pm[hd + GQ * j]);
+    float L = 0.f, o = 0.f;
+    if (M != -INFINITY) {
+#pragma unroll
+      for (int j = 0; j < WPH; ++j) {
+        const float wj = exp2f(pm[hd + GQ * j] - M);
+        L = fmaf(pl[hd + GQ * j], wj, L);
+        o = fmaf(po[hd + GQ * j][c], wj, o);
+      }
     }
-    if (lane == 0) {
-      if (seg) v += p.seg_o[(size_t)row * kD + cp] * sw;
-      const size_t idx = (size_t)row * kD + cp;
-      if (out_fp32) static_cast<float*>(out)[idx] = v;
-      else static_cast<__nv_bfloat16*>(out)[idx] = __float2bfloat16_rn(v);
+    const float wseg = (seg && M != -INFINITY) ? exp2f(p.seg_m[row] - M) : 0.f;
+    if (seg) L = fmaf(p.seg_l[row], wseg, L);
+    const float inv = L > 0.f ? 1.f / L : 0.f;
+    ot[hd][c] = o * inv;
+    if (c == 0) {
+      sws[hd] = wseg * inv;
+      if (lse) lse[row] = L > 0.f ? (M + log2f(L)) * 0.6931471805599453f : -INFINITY;
     }
+  }
+  __syncthreads();
+  const int cp = tid & (kD - 1), hh = tid >> 7;
+  float acc[HPT];
+  if (RV) {
+    asm volatile(
+        "{\n.reg .pred P1;\nWAIT_R%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n"
+        "@!P1 bra WAIT_R%=;\n}\n" ::"r"(msmem_u32(&bar))
+        : "memory");
+#pragma unroll
+    for (int j = 0; j < HPT; ++j) acc[j] = 0.f;
+    const float4* Rrow = reinterpret_cast<const float4*>(Rs + (size_t)cp * kD);
+#pragma unroll 8
+    for (int k = 0; k < kD / 4; ++k) {
+      const int c4 = (k + lane) & 31;
+      const float4 r = Rrow[c4];
+#pragma unroll
+      for (int j = 0; j < HPT; ++j) {
+        const int hd = hh + 2 * j;
+        if (hd < GQ) {
+          const float4 x = reinterpret_cast<const float4*>(ot[hd])[c4];
+          acc[j] = fmaf(r.x, x.x, fmaf(r.y, x.y, fmaf(r.z, x.z, fmaf(r.w, x.w, acc[j]))));
+        }
+      }
+    }
+  } else {                                           // pre-rotated V (NEXT-2): o = õ
+#pragma unroll
+    for (int j = 0; j < HPT; ++j) acc[j] = hh + 2 * j < GQ ? ot[hh + 2 * j][cp] : 0.f;
+  }
+#pragma unroll
+  for (int j = 0; j < HPT; ++j) {
+    const int hd = hh + 2 * j;
+    if (hd >= GQ) continue;
+    const size_t row = (size_t)b * p.hq + (size_t)h * GQ + hd;
+    float v = acc[j];
+    if (seg) v = fmaf(p.seg_o[row * kD + cp], sws[hd], v);
+    const size_t idx = row * kD + cp;
+    if (out_fp32) static_cast<float*>(out)[idx] = v;
+    else static_cast<__nv_bfloat16*>(out)[idx] = __float2bfloat16_rn(v);
   }
 }
 
@@ -539,7 +632,8 @@ cudaError_t launch_attend(const oscar_ctx& c, const void* q, const int32_t* page
     pp.q = static_cast<const uint16_t*>(q); pp.RK = RK; pp.RV = RV;
     pp.Hq = c.hq; pp.lgG = lgG; pp.bits = c.bits; pp.nt = p.nt; pp.qscale = c.scale * kLog2e;
     pp.qt = p.qt; pp.qint = p.qint; pp.qsc = p.qscale; pp.qsum = p.qsum;
-    pp.qfrag = mma ? p.qfrag : nullptr; pp.work = mma ? p.work : nullptr;
+    pp.qfrag = mma ? p.qfrag : nullptr;
+    pp.tq = mma && attend_mma_tq(c) ? 1 : 0; pp.work = mma ? p.work : nullptr;
     pp.knew = static_cast<const uint16_t*>(k_new); pp.vnew = static_cast<const uint16_t*>(v_new);
     pp.page_table = page_table; pp.seq_lens = seq_lens; pp.max_pages = max_pages;
     pp.pool = static_cast<uint8_t*>(const_cast<void*>(pool));
@@ -577,18 +671,25 @@ cudaError_t launch_attend(const oscar_ctx& c, const void* q, const int32_t* page
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
+#ifndef OSCAR_SKIP_MERGE   // (A/B builds only: measures the merge's share of attend)
   {
-    const int msmem = p.n_splits * 4;
+    void (*fn)(AttnParams, const float*, void*, int, float*) =
+        c.g == 1 ? attend_merge_kernel<1> : c.g == 2 ? attend_merge_kernel<2>
+      : c.g == 4 ? attend_merge_kernel<4> : attend_merge_kernel<8>;
+    const int msmem = RV ? kD * kD * 4 : 0;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, msmem);
+    if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3((unsigned)(B * c.hq));
-    cfg.blockDim = dim3(512);
+    cfg.gridDim = dim3((unsigned)B, (unsigned)c.hkv);
+    cfg.blockDim = dim3(256);
     cfg.dynamicSmemBytes = msmem;
     cfg.stream = s;
     cfg.attrs = pdl;
     cfg.numAttrs = OSCAR_PDL_MERGE;
-    e = cudaLaunchKernelEx(&cfg, attend_merge_kernel, p, RV, out, out_fp32, lse);
+    e = cudaLaunchKernelEx(&cfg, fn, p, RV, out, out_fp32, lse);
     if (e != cudaSuccess) return e;
   }
+#endif
   return cudaGetLastError();
 }
 

@@ -31,6 +31,7 @@ struct AttnParams {
 };
 
 bool attend_mma_supported(const oscar_ctx& c);
+bool attend_mma_tq(const oscar_ctx& c);      // the partial kernel uses the token-row QK layout
 
 // IMMA QK k-slot -> channel map (see attend_mma.cu): in K-step kk (0..3), lane t's B
 // registers hold channels 32t .. 32t+31 of the token row; slot = 4t + m (+16 for b1).

@@ -46,11 +46,23 @@ constexpr int kWarps = 4;
 #ifndef OSCAR_MINB
 #define OSCAR_MINB 4
 #endif
+#ifndef OSCAR_TQ
+#define OSCAR_TQ 1      // token-row QK layout where it applies (A/B: -DOSCAR_TQ=0)
+#endif
 
 
 __device__ __forceinline__ void imma16832(int (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
   asm volatile(
       "mma.sync.aligned.m16n8k32.row.col.s32.s8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// A unsigned (codes), B signed (q̃): the token-row QK layout
+__device__ __forceinline__ void imma16832_us(int (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
       "{%0,%1,%2,%3};\n"
       : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
@@ -68,6 +80,11 @@ __device__ __forceinline__ float ex2_ftz(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;\n" : "=f"(y) : "f"(x));
   return y;
+}
+
+__device__ __forceinline__ uint32_t hmul2_u32(uint32_t a, uint32_t b) {
+  const __half2 r = __hmul2(*reinterpret_cast<const __half2*>(&a), *reinterpret_cast<const __half2*>(&b));
+  return *reinterpret_cast<const uint32_t*>(&r);
 }
 
 __device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
@@ -166,9 +183,11 @@ __device__ __forceinline__ Item decode_item(const AttnParams& p, int it) {
 
 }  // namespace
 
-template <int BITS, int GQ, int NG>
+template <int BITS, int GQ, int NG, bool TQ>
 __global__ void __launch_bounds__(kWarps * 32, (GQ * NG <= 8 ? OSCAR_MINB : OSCAR_MINB_NT2))
 attend_partial_mma(AttnParams p, int S) {
+  static_assert(!TQ || (BITS == 2 && NG <= 2 && GQ >= 2), "token-row QK layout: 2-bit, G >= 64, g >= 2");
+  constexpr int NTQ = (GQ + 3) / 4;           // TQ: QK N-tiles of 4 heads x (hi|lo)
   constexpr int NC = GQ * NG;                 // (group, head) combos
   constexpr int NT = (NC + 7) / 8;            // 8-combo tiles (QK M-tiles / PV N-tiles)
   constexpr int kChunk = NT > 1 ? OSCAR_CHUNK_NT2 : OSCAR_CHUNK;   // 16-token sub-tiles per softmax chunk
@@ -262,8 +281,11 @@ attend_partial_mma(AttnParams p, int S) {
       grp_of[j] = c < NC ? c / GQ : 0;
       qsumf[j] = c < NC ? (float)p.qsum[qrow * 8 + grp_of[j]] * kBScale : 0.f;
     }
-    uint32_t aq[NT][4][4];
-    {
+    // QK operand fragments of this (b, h), built by the prologue kernel: A (q rows, TQ = false)
+    // or B (q columns, TQ = true)
+    uint32_t aq[TQ ? 1 : NT][4][4];
+    uint32_t bq[TQ ? NTQ : 1][4][2];
+    if constexpr (!TQ) {
       const uint32_t* qf = p.qfrag + ((size_t)I.b * p.hkv + I.h) * NT * 16 * 32 + lane;
 #pragma unroll
       for (int j = 0; j < NT; ++j)
@@ -271,21 +293,48 @@ attend_partial_mma(AttnParams p, int S) {
         for (int kk = 0; kk < 4; ++kk)
 #pragma unroll
           for (int r = 0; r < 4; ++r) aq[j][kk][r] = qf[(j * 16 + kk * 4 + r) * 32];
+    } else {
+      const uint32_t* qf = p.qfrag + ((size_t)I.b * p.hkv + I.h) * NTQ * 8 * 32 + lane;
+#pragma unroll
+      for (int jt = 0; jt < NTQ; ++jt)
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+          for (int r = 0; r < 2; ++r) bq[jt][kk][r] = qf[(jt * 8 + kk * 2 + r) * 32];
+    }
+    // TQ: this lane's heads in the score layout are hq = 4·jt + t
+    float qscale_h[NTQ], qs_h[NTQ][NG];
+    if constexpr (TQ) {
+#pragma unroll
+      for (int jt = 0; jt < NTQ; ++jt) {
+        const int hq = 4 * jt + t;
+        const size_t row = (size_t)I.b * p.hq + (size_t)I.h * GQ + hq;
+        qscale_h[jt] = hq < GQ ? p.qscale[row] * (1.f / kBScale) : 0.f;
+#pragma unroll
+        for (int g = 0; g < NG; ++g) qs_h[jt][g] = hq < GQ ? (float)p.qsum[row * 8 + g] * kBScale : 0.f;
+      }
     }
     float acc[8][NT][4];
     f2 mv2[NT];                               // Σ p·m_V of this lane's combo over its tokens (2 partial sums)
+    float accm[TQ ? NT : 1][4];               // TQ: Σ p·m_V through the tensor core (rows all equal)
 #pragma unroll
     for (int j = 0; j < NT; ++j) {
       mv2[j] = f2{0.f, 0.f};
 #pragma unroll
-      for (int e = 0; e < 4; ++e)
+      for (int e = 0; e < 4; ++e) {
+        if constexpr (TQ) accm[j][e] = 0.f;
 #pragma unroll
         for (int i = 0; i < 8; ++i) acc[i][j][e] = 0.f;
+      }
     }
     // scores are kept relative to m_run (log2 domain); m_run starts at 0 and the first chunk
-    // of the item moves it to that chunk's max, later chunks only when the max grows by > 8
+    // of the item moves it to that chunk's max, later chunks only when the max grows
     float m_run = 0.f;
     f2 l2{0.f, 0.f};                          // Σ p of this lane's tokens (2 partial sums)
+    float m_h[NTQ];                           // TQ: per head of this lane
+    f2 l_h[NTQ];
+#pragma unroll
+    for (int jt = 0; jt < NTQ; ++jt) { m_h[jt] = 0.f; l_h[jt] = f2{0.f, 0.f}; }
     bool fresh = true;
 
     // one page: chunks of up to 4 sub-tiles (64 tokens)
@@ -464,12 +513,197 @@ attend_partial_mma(AttnParams p, int S) {
       }
     };
 
+    // TQ page body: QK with the tokens as the MMA rows.  A = K codes of K-tile rows gid /
+    // gid + 8 (tokens 2·gid, 2·gid + 1 of the 16-token sub-tile, FORMAT fmt_krow), lane t taking
+    // words t and 4 + t of each row so every 32-channel k-step stays inside one quantization
+    // group (G >= 64) and accumulates into that group's C; B = q̃ hi/lo int8 columns (4 heads x
+    // (hi|lo) per N-tile).  Each lane then owns the scores of its two tokens for head 4·jt + t —
+    // no cross-group shuffles, no duplicated softmax.  PV is the kernel's usual HMMA with the
+    // B operand gathered by two shuffles (p pairs as half2) and formed by HMUL2 with s_V; the
+    // Σ p·m_V term runs as an extra HMMA against an all-ones A tile.
+    auto page_body_tq = [&](const unsigned char* pg, int valid, auto full_c) {
+      constexpr int FULLSUB = decltype(full_c)::value;
+      constexpr bool FULL = FULLSUB > 0;
+      const unsigned char* vcodes = pg + (FULL ? 64 * RB : p.vcodes_off);
+      const unsigned char* meta = pg + (FULL ? 128 * RB : p.meta_off);
+      const int n_sub = FULL ? FULLSUB : ((valid + 15) >> 4);
+      const int hc = gid % GQ;                  // PV: head of this lane's combo column(s)
+      for (int c0 = 0; c0 < n_sub; c0 += kChunk) {
+        float sc[kChunk][NTQ][2];
+        float tmax[NTQ];
+#pragma unroll
+        for (int jt = 0; jt < NTQ; ++jt) tmax[jt] = -INFINITY;
+#pragma unroll
+        for (int sl = 0; sl < kChunk; ++sl) {
+          const int st = c0 + sl;
+          if (st >= n_sub) {
+#pragma unroll
+            for (int jt = 0; jt < NTQ; ++jt) sc[sl][jt][0] = sc[sl][jt][1] = -INFINITY;
+            continue;
+          }
+          const uint32_t* ra = reinterpret_cast<const uint32_t*>(pg + (size_t)(16 * st + gid) * RB);
+          const uint32_t* rb = reinterpret_cast<const uint32_t*>(pg + (size_t)(16 * st + 8 + gid) * RB);
+          const uint32_t wa[2] = {ra[t], ra[4 + t]}, wb[2] = {rb[t], rb[4 + t]};
+          int cq[NTQ][NG][4];
+#pragma unroll
+          for (int jt = 0; jt < NTQ; ++jt)
+#pragma unroll
+            for (int g = 0; g < NG; ++g)
+#pragma unroll
+              for (int e = 0; e < 4; ++e) cq[jt][g][e] = 0;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            // k-step kk: word kk/2 (group kk/2 when G = 64), 2-bit fields 2(kk&1) (a0, a1) and
+            // 2(kk&1)+1 (a2, a3) moved to the top of each byte (c·64, folded into qscale)
+            const int wi = kk >> 1, s0 = 6 - 4 * (kk & 1);
+            uint32_t a[4];
+            a[0] = (wa[wi] << s0) & 0xC0C0C0C0u;
+            a[1] = (wb[wi] << s0) & 0xC0C0C0C0u;
+            a[2] = (wa[wi] << (s0 - 2)) & 0xC0C0C0C0u;
+            a[3] = (wb[wi] << (s0 - 2)) & 0xC0C0C0C0u;
+            const int g = NG == 2 ? (kk >> 1) : 0;
+#pragma unroll
+            for (int jt = 0; jt < NTQ; ++jt) imma16832_us(cq[jt][g], a, bq[jt][kk][0], bq[jt][kk][1]);
+          }
+          // scores of tokens 2·gid (e = 0) and 2·gid + 1 (e = 1) for head 4·jt + t
+#pragma unroll
+          for (int jt = 0; jt < NTQ; ++jt) {
+            f2 part{0.f, 0.f};
+#pragma unroll
+            for (int g = 0; g < NG; ++g) {
+              const uint2 mk = *reinterpret_cast<const uint2*>(meta + 128 * NG * st + 128 * g + 32 * (gid >> 1) + 8 * (gid & 1));
+              f2 sk, mq;
+              halves_f2(mk.x, mk.y, sk, mq);
+              const int d0 = cq[jt][g][0] * 256 + cq[jt][g][1];
+              const int d1 = cq[jt][g][2] * 256 + cq[jt][g][3];
+              part = ffma2(sk, f2{(float)d0, (float)d1}, ffma2(mq, f2{qs_h[jt][g], qs_h[jt][g]}, part));
+            }
+            const f2 v = ffma2(part, f2{qscale_h[jt], qscale_h[jt]}, f2{-m_h[jt], -m_h[jt]});
+            sc[sl][jt][0] = v.x;
+            sc[sl][jt][1] = v.y;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              bool ok = 4 * jt + t < GQ;
+              if (!FULL) ok = ok && (16 * st + 2 * gid + e) < valid;
+              if (!ok) sc[sl][jt][e] = -INFINITY;
+              tmax[jt] = fmaxf(tmax[jt], sc[sl][jt][e]);
+            }
+          }
+        }
+        bool need_any = false;
+        float alpha[NTQ];
+        const bool first = fresh;
+        fresh = false;
+#pragma unroll
+        for (int jt = 0; jt < NTQ; ++jt) {
+#pragma unroll
+          for (int o = 4; o < 32; o <<= 1) tmax[jt] = fmaxf(tmax[jt], __shfl_xor_sync(0xffffffffu, tmax[jt], o));
+          const bool need = first ? tmax[jt] > -INFINITY : tmax[jt] > (float)OSCAR_LAZY;
+          const float shift = need ? tmax[jt] : 0.f;
+          alpha[jt] = first ? 1.f : ex2_ftz(-shift);
+          if (need) {
+#pragma unroll
+            for (int sl = 0; sl < kChunk; ++sl) { sc[sl][jt][0] -= shift; sc[sl][jt][1] -= shift; }
+            m_h[jt] += shift;
+            l_h[jt] = fmul2(l_h[jt], f2{alpha[jt], alpha[jt]});
+          }
+          need_any = need_any || (need && !first);
+        }
+        if (__any_sync(0xffffffffu, need_any)) {
+          // accumulator column (combo 8j + 2t + e) of head (8j + 2t + e) % GQ: its alpha lives
+          // in lane t' = head % 4, slot head / 4
+#pragma unroll
+          for (int j = 0; j < NT; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int hq = (8 * j + 2 * t + e) % GQ;
+              float a = __shfl_sync(0xffffffffu, alpha[0], hq & 3);
+              if (NTQ > 1) {
+                const float a1 = __shfl_sync(0xffffffffu, alpha[NTQ - 1], hq & 3);
+                a = hq >= 4 ? a1 : a;
+              }
+              accm[j][e] *= a; accm[j][e + 2] *= a;
+#pragma unroll
+              for (int i = 0; i < 8; ++i) { acc[i][j][e] *= a; acc[i][j][e + 2] *= a; }
+            }
+        }
+        // ---- PV per sub-tile
+#pragma unroll
+        for (int sl = 0; sl < kChunk; ++sl) {
+          const int st = c0 + sl;
+          if (st >= n_sub) break;
+          uint32_t P[NTQ];
+#pragma unroll
+          for (int jt = 0; jt < NTQ; ++jt) {
+            const float p0 = ex2_ftz(sc[sl][jt][0]), p1 = ex2_ftz(sc[sl][jt][1]);   // exp2(-inf) = 0
+            l_h[jt] = fadd2(l_h[jt], f2{p0, p1});
+            P[jt] = pack_half2(p0, p1);
+          }
+          // (p(4t), p(4t+1)) from lane (2t, hc%4), (p(4t+2), p(4t+3)) from lane (2t+1, hc%4)
+          uint32_t X = __shfl_sync(0xffffffffu, P[0], 8 * t + (hc & 3));
+          uint32_t Y = __shfl_sync(0xffffffffu, P[0], 8 * t + 4 + (hc & 3));
+          if (NTQ > 1) {
+            const uint32_t X1 = __shfl_sync(0xffffffffu, P[NTQ - 1], 8 * t + (hc & 3));
+            const uint32_t Y1 = __shfl_sync(0xffffffffu, P[NTQ - 1], 8 * t + 4 + (hc & 3));
+            if (hc >= 4) { X = X1; Y = Y1; }
+          }
+          const uint32_t p02 = __byte_perm(X, Y, 0x5410), p13 = __byte_perm(X, Y, 0x7632);
+          uint32_t bpv[NT][2];
+#pragma unroll
+          for (int j = 0; j < NT; ++j) {
+            const int gc = min((8 * j + gid) / GQ, NG - 1);
+            const uint4 mv4 = *reinterpret_cast<const uint4*>(meta + 128 * NG * st + 128 * gc + 32 * t + 16);
+            uint32_t mw[4] = {mv4.x, mv4.y, mv4.z, mv4.w};
+            if (!FULL) {   // masked tokens may carry garbage metadata: keep them out
+#pragma unroll
+              for (int e = 0; e < 4; ++e) mw[e] = (16 * st + 4 * t + e) < valid ? mw[e] : 0u;
+            }
+            const uint32_t s02 = __byte_perm(mw[0], mw[2], 0x5410), s13 = __byte_perm(mw[1], mw[3], 0x5410);
+            const uint32_t m02 = __byte_perm(mw[0], mw[2], 0x7632), m13 = __byte_perm(mw[1], mw[3], 0x7632);
+            bpv[j][0] = hmul2_u32(p02, s02);   // k-slots 2t, 2t+1 <-> tokens 4t, 4t+2
+            bpv[j][1] = hmul2_u32(p13, s13);   // k-slots 2t+8, 2t+9 <-> tokens 4t+1, 4t+3
+            const uint32_t ones[4] = {0x3C003C00u, 0x3C003C00u, 0x3C003C00u, 0x3C003C00u};
+            hmma16816(accm[j], ones, hmul2_u32(p02, m02), hmul2_u32(p13, m13));
+          }
+          uint32_t vw[VW];
+          {
+            const uint4* vp = reinterpret_cast<const uint4*>(vcodes + (size_t)st * 16 * RB) + 4 * gid + t;
+#pragma unroll
+            for (int u = 0; u < VW / 4; ++u) {
+              const uint4 x = vp[32 * u];
+              vw[4 * u] = x.x; vw[4 * u + 1] = x.y; vw[4 * u + 2] = x.z; vw[4 * u + 3] = x.w;
+            }
+          }
+          uint32_t vs[VW];
+#pragma unroll
+          for (int k = 0; k < VW; ++k) vs[k] = vw[k] >> 8;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int q = i % CPB;
+            const uint32_t msk = kCodeMask << (BITS * q);
+            uint32_t a[4];
+            a[0] = vw[i / CPB] & msk;
+            a[1] = vw[VW / 2 + i / CPB] & msk;
+            a[2] = vs[i / CPB] & msk;
+            a[3] = vs[VW / 2 + i / CPB] & msk;
+#pragma unroll
+            for (int j = 0; j < NT; ++j) hmma16816(acc[i][j], a, bpv[j][0], bpv[j][1]);
+          }
+        }
+      }
+    };
+
     for (int k = 0; k < I.np; ++k) {
       mbar_wait(&bars[s_use], ph_use);
       const unsigned char* pg = ring + (size_t)s_use * page_bytes;
       const int valid = min(P, I.seq_len - (I.page0 + k) * P);
-      if (valid == 64 && P == 64) page_body(pg, valid, std::integral_constant<int, 4>{});
-      else page_body(pg, valid, std::integral_constant<int, 0>{});
+      if constexpr (TQ) {
+        if (valid == 64 && P == 64) page_body_tq(pg, valid, std::integral_constant<int, 4>{});
+        else page_body_tq(pg, valid, std::integral_constant<int, 0>{});
+      } else {
+        if (valid == 64 && P == 64) page_body(pg, valid, std::integral_constant<int, 4>{});
+        else page_body(pg, valid, std::integral_constant<int, 0>{});
+      }
       // release the stage (every lane's reads are done) and refill it
       __syncwarp();
       if (++s_use == S) { s_use = 0; ph_use ^= 1u; }
@@ -481,6 +715,13 @@ attend_partial_mma(AttnParams p, int S) {
     float l_run = l2.x + l2.y;
     l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
     l_run += __shfl_xor_sync(0xffffffffu, l_run, 2);
+    float l_hd[NTQ];                          // TQ: Σ p of head 4·jt + t over the 8 gid lanes
+#pragma unroll
+    for (int jt = 0; jt < NTQ; ++jt) {
+      l_hd[jt] = l_h[jt].x + l_h[jt].y;
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) l_hd[jt] += __shfl_xor_sync(0xffffffffu, l_hd[jt], o);
+    }
     float mv_acc[NT];
 #pragma unroll
     for (int j = 0; j < NT; ++j) {
@@ -495,7 +736,8 @@ attend_partial_mma(AttnParams p, int S) {
       for (int e = 0; e < 4; ++e) {
         const int col = 2 * t + (e & 1);
         const int cc = 8 * j + col;
-        const float mvs = __shfl_sync(0xffffffffu, mv_acc[j], 4 * col);   // combo col = gid of lane 4·col
+        const float mvs = TQ ? accm[j][e & 1]                               // this lane's column
+                             : __shfl_sync(0xffffffffu, mv_acc[j], 4 * col);   // combo col = gid of lane 4·col
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const float unscale = (float)(1 << (24 - BITS * (i % CPB)));
@@ -506,7 +748,15 @@ attend_partial_mma(AttnParams p, int S) {
           }
         }
       }
-    if (t == 0 && gid < GQ) {
+    if constexpr (TQ) {
+#pragma unroll
+      for (int jt = 0; jt < NTQ; ++jt)
+        if (gid == 0 && 4 * jt + t < GQ) {
+          const size_t row = row0 + (size_t)(4 * jt + t) * p.n_splits;
+          p.ws_m[row] = I.np > 0 ? m_h[jt] : -INFINITY;
+          p.ws_l[row] = l_hd[jt];
+        }
+    } else if (t == 0 && gid < GQ) {
       const size_t row = row0 + (size_t)gid * p.n_splits;
       p.ws_m[row] = I.np > 0 ? m_run : -INFINITY;
       p.ws_l[row] = l_run;
@@ -530,7 +780,7 @@ using KernelFn = void (*)(AttnParams, int);
 template <int BITS>
 KernelFn pick_g(int g, int ng) {
 #define OSCAR_CASE(GQ_, NG_) \
-  if (g == GQ_ && ng == NG_) return attend_partial_mma<BITS, GQ_, NG_>;
+  if (g == GQ_ && ng == NG_) return attend_partial_mma<BITS, GQ_, NG_, false>;
   OSCAR_CASE(1, 1) OSCAR_CASE(1, 2) OSCAR_CASE(1, 4)
   OSCAR_CASE(2, 1) OSCAR_CASE(2, 2) OSCAR_CASE(2, 4)
   OSCAR_CASE(4, 1) OSCAR_CASE(4, 2) OSCAR_CASE(4, 4)
@@ -539,7 +789,19 @@ KernelFn pick_g(int g, int ng) {
   return nullptr;
 }
 
+// token-row QK layout (TQ): 2-bit codes, G in {64, 128}, g in {2, 4, 8}
+KernelFn pick_tq(int g, int ng) {
+#define OSCAR_CASE(GQ_, NG_) \
+  if (g == GQ_ && ng == NG_) return attend_partial_mma<2, GQ_, NG_, true>;
+  OSCAR_CASE(2, 1) OSCAR_CASE(2, 2) OSCAR_CASE(4, 1) OSCAR_CASE(4, 2) OSCAR_CASE(8, 1) OSCAR_CASE(8, 2)
+#undef OSCAR_CASE
+  return nullptr;
+}
+
 KernelFn pick(int bits, int g, int ng) {
+  if (bits == 2 && OSCAR_TQ) {
+    if (KernelFn f = pick_tq(g, ng)) return f;
+  }
   if (bits == 2) return pick_g<2>(g, ng);
   if (bits == 4) return pick_g<4>(g, ng);
   return nullptr;
@@ -550,6 +812,8 @@ int stages_for(int page_bytes) {
   return S < 2 ? 2 : (S > 4 ? 4 : S);
 }
 }  // namespace
+
+bool attend_mma_tq(const oscar_ctx& c) { return OSCAR_TQ && c.bits == 2 && pick_tq(c.g, c.ng) != nullptr; }
 
 bool attend_mma_supported(const oscar_ctx& c) {
   return c.d == 128 && pick(c.bits, c.g, c.ng) != nullptr && c.P % 16 == 0;

@@ -71,6 +71,19 @@ __global__ void __launch_bounds__(512) attend_prologue_kernel(PrologueParams pp)
   const int G = 1 << pp.lgG;
   const bool dec = pp.knew != nullptr;
   if (pp.work && b == 0 && h == 0 && tid == 0) *pp.work = 0;   // reset the work-item counter
+  // this warp's 8 rows of R_K (and R_V) are loaded first: their latency overlaps the row loads
+  const bool rv = dec && pp.RV;
+  float4 rk[8], rvv[8];
+  {
+    const float4* RK4 = reinterpret_cast<const float4*>(pp.RK + (size_t)h * kD * kD) + (size_t)8 * w * 32 + lane;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) rk[i] = __ldg(RK4 + i * 32);
+    if (rv) {
+      const float4* RV4 = reinterpret_cast<const float4*>(pp.RV + (size_t)h * kD * kD) + (size_t)8 * w * 32 + lane;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) rvv[i] = __ldg(RV4 + i * 32);
+    }
+  }
   for (int e = tid; e < NR * (kD / 4); e += 512) {
     const int r = e >> 5, l4 = e & 31;
     const uint16_t* src = r < GQ ? pp.q + ((size_t)b * pp.Hq + (size_t)h * GQ + r) * kD
@@ -85,17 +98,6 @@ __global__ void __launch_bounds__(512) attend_prologue_kernel(PrologueParams pp)
   }
   __syncthreads();
   {
-    const float4* RK4 = reinterpret_cast<const float4*>(pp.RK + (size_t)h * kD * kD) + (size_t)8 * w * 32 + lane;
-    const bool rv = dec && pp.RV;
-    const float4* RV4 = rv ? reinterpret_cast<const float4*>(pp.RV + (size_t)h * kD * kD) + (size_t)8 * w * 32 + lane
-                           : nullptr;
-    float4 rk[8], rvv[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) rk[i] = __ldg(RK4 + i * 32);
-    if (rv) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) rvv[i] = __ldg(RV4 + i * 32);
-    }
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
       if (r > GQ && !rv) break;

@@ -541,9 +541,16 @@ attend_partial_mma(AttnParams p, int S) {
             for (int jt = 0; jt < NTQ; ++jt) sc[sl][jt][0] = sc[sl][jt][1] = -INFINITY;
             continue;
           }
-          const uint32_t* ra = reinterpret_cast<const uint32_t*>(pg + (size_t)(16 * st + gid) * RB);
-          const uint32_t* rb = reinterpret_cast<const uint32_t*>(pg + (size_t)(16 * st + 8 + gid) * RB);
-          const uint32_t wa[2] = {ra[t], ra[4 + t]}, wb[2] = {rb[t], rb[4 + t]};
+          // one ldmatrix.x4: matrices (rows 0-7 | 8-15) x (bytes 0-15 | 16-31) of the K tile, so
+          // lane (gid, t) receives words t and 4 + t of rows gid and gid + 8
+          uint32_t wa[2], wb[2];
+          {
+            const int mi = lane >> 3;
+            const uint32_t addr = smem_u32(pg + (size_t)(16 * st + 8 * (mi >> 1) + (lane & 7)) * RB + 16 * (mi & 1));
+            asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];\n"
+                         : "=r"(wa[0]), "=r"(wa[1]), "=r"(wb[0]), "=r"(wb[1])
+                         : "r"(addr));
+          }
           int cq[NTQ][NG][4];
 #pragma unroll
           for (int jt = 0; jt < NTQ; ++jt)

@@ -216,8 +216,66 @@ def c4_leg(args, world, rank, dev, gen, RK_all, RV_all, hbm_peak, peak_kind):
             "GBps_aggregate": rank_bytes * world / ms / 1e6,
             "roofline": {"bound": "hbm", "achieved": rank_bytes / ms / 1e6, "peak": hbm_peak, "unit": "GB/s",
                          "frac": rank_bytes / ms / 1e6 / hbm_peak, "traffic": None,
-                         "kernel": "oscar_attend (q_rotate+partial+merge), g = 8",
+                         "kernel": "oscar_attend (prologue+partial+merge), g = 8",
                          "algorithmic_bytes_per_launch": rank_bytes, "peak_kind": peak_kind}}
+
+
+def c5_leg(args, dev, hbm_peak):
+    """b in {2,3,4} x G in {32,64,128} x B in {1,16,64,256} decode at L = 32768
+    (Llama-3-8B shape, random packed pools of the page FORMAT), and prefill-append of 4096 tokens
+    per sequence for B in {1, 16, 64}.  Median of 7 calls after 2 warm-up calls."""
+    import torch
+    from paper_2605_17757_b200 import binding as Bnd
+    from paper_2605_17757_b200 import synth
+    gen = torch.Generator(device=dev).manual_seed(4)
+    L, pts = 32768, []
+
+    def med(fn, reps=7):
+        for _ in range(2):
+            fn()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+        for a, b in ev:
+            a.record(); fn(); b.record()
+        torch.cuda.synchronize()
+        return sorted(a.elapsed_time(b) for a, b in ev)[reps // 2]
+
+    RK, RV = synth.torch_rotation(gen, HKV, D, dev), synth.torch_rotation(gen, HKV, D, dev)
+    for bits in (2, 3, 4):
+        for g in (32, 64, 128):
+            o = Bnd.Oscar(Bnd.Config(num_q_heads=HQ, num_kv_heads=HKV, bits=bits, group_size=g, page_size=P))
+            o.set_variant(args.variant)
+            tok_b = 2 * (D * bits // 8 + 4 * (D // g))
+            for B in (1, 16, 64, 256):
+                mp = L // P
+                pool = synth.torch_random_pool(gen, B * mp, HKV, o.page_bytes(), 2 * P * (D * bits // 8),
+                                               P * (D // g), dev)
+                pt = torch.randperm(B * mp, generator=gen, device=dev).to(torch.int32).reshape(B, mp).contiguous()
+                seq = torch.full((B,), L, dtype=torch.int32, device=dev)
+                q = synth.torch_decode_q(gen, B, HQ, D, dev)
+                ws = torch.empty(o.attend_workspace_bytes(B, mp), dtype=torch.uint8, device=dev)
+                out = torch.empty((B, HQ, D), dtype=torch.bfloat16, device=dev)
+                ms = med(lambda: o.attend(q, pt, seq, pool, RK, RV, ws, out))
+                byt = B * L * HKV * tok_b + 2 * B * HQ * D * 2
+                pts.append({"leg": "decode", "bits": bits, "G": g, "B": B, "L": L, "us": ms * 1e3,
+                            "GBps": byt / ms / 1e6, "frac": byt / ms / 1e6 / hbm_peak})
+                del pool
+                if B <= 64:
+                    T = B * 4096
+                    K, V = synth.torch_keys(gen, T, HKV, D, dev), synth.torch_values(gen, T, HKV, D, dev)
+                    npg = B * 4096 // P
+                    pool = torch.empty((npg, HKV, o.page_bytes()), dtype=torch.uint8, device=dev)
+                    slots = torch.randperm(npg, generator=gen, device=dev).repeat_interleave(P) * P + \
+                        torch.arange(P, device=dev).repeat(npg)
+                    ms = med(lambda: o.quantize_append(K, V, slots, RK, RV, pool))
+                    byt = T * HKV * (2 * D * 2 + tok_b + 8 // HKV)
+                    pts.append({"leg": "prefill_append", "bits": bits, "G": g, "B": B, "tokens": T,
+                                "us": ms * 1e3, "tokens_per_s": T / ms * 1e3, "GBps": byt / ms / 1e6,
+                                "frac": byt / ms / 1e6 / hbm_peak})
+                    del pool, K, V
+            torch.cuda.synchronize()
+    return {"config": "C5 sweep (SURVEY §8(d)): Llama-3-8B shape (32 q / 8 kv heads, d 128), page 64; decode "
+                      "attend at L = 32768 over random packed pools; prefill-append 4096 tokens per sequence "
+                      "into randomly placed pages", "peak_GBps": hbm_peak, "points": pts}
 
 
 # ------------------------------------------------------------------ GPU arm
@@ -232,6 +290,7 @@ def main():
     ap.add_argument("--no-extras", action="store_true", help="skip calibration / prefill / e2e / cpu legs (ncu runs)")
     ap.add_argument("--no-c4", action="store_true", help="skip the C4 (Llama-3-70B-shaped, 128k) decode leg")
     ap.add_argument("--c4-only", action="store_true", help="run only the C4 decode leg and print its dict")
+    ap.add_argument("--c5-only", action="store_true", help="run only the C5 sweep (bits x G x B) and print it")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -252,6 +311,10 @@ def main():
     from paper_2605_17757_b200.parallel import allreduce_covariances, barrier, max_over_ranks
 
     hbm_peak, _, peak_kind = measured_peaks()
+    if args.c5_only:
+        if rank == 0:
+            print(json.dumps(c5_leg(args, dev, hbm_peak)), flush=True)
+        return
     if args.c4_only:
         gen = torch.Generator(device=dev).manual_seed(1234 + rank)
         RK = torch.stack([synth.torch_rotation(gen, HKV, D, dev) for _ in range(C4_LAYERS)])

@@ -13,7 +13,8 @@
 //               (reading Z4: one FFMA + bit clamp per code), pack, store into the slot's page
 //               block (FORMAT, common.cuh); V codes of whole 16-token tiles are staged in smem in
 //               FORMAT order and written as 16-B chunks.
-// Scope of this kernel: b in {2, 4}, G in {32, 64}, no clipping; other configs use the simple
+// Scope of this kernel: b in {2, 4}, G in {32, 64, 128} (a G = 128 group spans the two channel
+// halves: the two warps swap min/max through smem), no clipping; other configs use the simple
 // kernel (append.cu).
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -40,6 +41,7 @@ struct TcSmem {
   alignas(1024) uint8_t Blo[kBBytes];
   alignas(1024) uint8_t A[kStages][kTileBytes]; // [stage][2 k-chunks][128 rows tok][128 B]
   alignas(16) uint8_t vstage[2][4][kVStage];    // per (tile parity, lane quarter): FORMAT-ordered V codes
+  float2 xch[2][2][4][2][32];                   // G = 128: (buffer, parity, quarter, half, lane) min/max
   uint64_t full[kStages], empty[kStages], tfull[2], tempty[2];
   uint32_t tmem_base;
 };
@@ -222,7 +224,9 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
     const int par = ew >> 3;                      // tiles i with i % 2 == par (accumulator par)
     const int r = quarter * 32 + lane;            // row (token) within the tile
     constexpr int QMAX = (1 << BITS) - 1;
-    constexpr int GPH = 64 / G;                   // groups in this half
+    constexpr int GH = G < 64 ? G : 64;           // channels of a group inside this half
+    constexpr int GPH = 64 / GH;                  // groups (or group halves, G = 128) in this half
+    int xbuf = 0;
     // slot of this thread's token, loaded one tile ahead (its latency is off the critical path)
     auto load_slot = [&](int i) -> int64_t {
       const int64_t tk = (int64_t)(sub + i * p.cpp) * kTok + r;
@@ -251,9 +255,10 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
       // so they take the same branch and meet at the same named barrier.
       const int64_t slot0 = __shfl_sync(0xffffffffu, slot, 0);
       const bool fastV = isV && __all_sync(0xffffffffu, valid && slot == slot0 + lane && (slot0 & 15) == 0);
-      if (!valid) continue;
-      const int64_t page = slot / p.P;
-      const int u = (int)(slot % p.P);
+      // (G = 128: rows past T still take part in the partner exchange below; they store nothing)
+      if (!valid && G != 128) continue;
+      const int64_t page = valid ? slot / p.P : 0;
+      const int u = valid ? (int)(slot % p.P) : 0;
       uint8_t* blk = p.pool + (page * p.hkv + h) * (int64_t)p.page_bytes;
       // codes: the magic add leaves float bits 0x4B400000 + code; accumulate bits << shift with
       // one LEA per code and remove the constant part once per word
@@ -262,30 +267,41 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
       for (int w = 0; w < BITS * 2; ++w) packed[w] = 0u - magic_words<BITS>();
 #pragma unroll
       for (int gi = 0; gi < GPH; ++gi) {
-        float mn = __uint_as_float(v[gi * G]), mx = mn;
+        float mn = __uint_as_float(v[gi * GH]), mx = mn;
 #pragma unroll
-        for (int c = 1; c < G; ++c) {
-          const float x = __uint_as_float(v[gi * G + c]);
+        for (int c = 1; c < GH; ++c) {
+          const float x = __uint_as_float(v[gi * GH + c]);
           mn = fminf(mn, x);
           mx = fmaxf(mx, x);
+        }
+        if (G == 128) {
+          // the group spans both channel halves: swap min/max with the partner warp (same rows)
+          S.xch[xbuf][par][quarter][half][lane] = make_float2(mn, mx);
+          asm volatile("bar.sync %0, 64;\n" ::"r"(1 + quarter + 4 * par) : "memory");
+          const float2 o = S.xch[xbuf][par][quarter][half ^ 1][lane];
+          mn = fminf(mn, o.x);
+          mx = fmaxf(mx, o.y);
+          xbuf ^= 1;
         }
         const float s = __fdiv_rn(__fsub_rn(mx, mn), (float)QMAX);
         const __half s16 = __float2half_rn(s), m16 = __float2half_rn(mn);
         const float sf = __half2float(s16), m = __half2float(m16);
         const float inv = sf > 0.f ? __fdiv_rn(1.f, sf) : 0.f;
 #pragma unroll
-        for (int c = 0; c < G; ++c) {
+        for (int c = 0; c < GH; ++c) {
           // reading Z4: rint(RN(x - m)·inv) with the exact product: one FFMA with the 1.5·2^23
           // magic constant (round-half-even), clamp on the float bits (same exponent)
-          const float tq = __fmaf_rn(__fsub_rn(__uint_as_float(v[gi * G + c]), m), inv, 12582912.f);
+          const float tq = __fmaf_rn(__fsub_rn(__uint_as_float(v[gi * GH + c]), m), inv, 12582912.f);
           const uint32_t bits = (uint32_t)min(max(__float_as_int(tq), 0x4B400000), 0x4B400000 + QMAX);
-          const int idx = gi * G + c;             // code index within the half row
+          const int idx = gi * GH + c;            // code index within the half row
           packed[idx * BITS / 32] += bits << ((idx * BITS) & 31);
         }
-        const int grp = (half * 64 + gi * G) / G;
-        *reinterpret_cast<__half2*>(blk + p.meta_off + fmt_meta(u, grp, p.ng) + (isV ? 16 : 0)) =
-            __halves2half2(s16, m16);
+        const int grp = (half * 64 + gi * GH) / G;
+        if (valid && (G < 128 || half == 0))
+          *reinterpret_cast<__half2*>(blk + p.meta_off + fmt_meta(u, grp, p.ng) + (isV ? 16 : 0)) =
+              __halves2half2(s16, m16);
       }
+      if (!valid) continue;
       constexpr int HB = 8 * BITS;                // bytes of this half row
       constexpr int RB = 16 * BITS;               // bytes of a row
       if (!isV) {
@@ -374,6 +390,8 @@ TcFn pick(int bits, int G) {
   if (bits == 2 && G == 32) return append_tc_kernel<2, 32>;
   if (bits == 4 && G == 64) return append_tc_kernel<4, 64>;
   if (bits == 4 && G == 32) return append_tc_kernel<4, 32>;
+  if (bits == 2 && G == 128) return append_tc_kernel<2, 128>;
+  if (bits == 4 && G == 128) return append_tc_kernel<4, 128>;
   return nullptr;
 }
 }  // namespace

@@ -814,16 +814,20 @@ KernelFn pick(int bits, int g, int ng) {
   return nullptr;
 }
 
+// ring stages per warp: 2-4 within ~48 KB per CTA; large pages (P = 256 at 4 bits: 36 KB) fall
+// back to what fits in the 227-KB CTA limit (1 stage), 0 if not even that
 int stages_for(int page_bytes) {
-  const int S = (48 * 1024) / (kWarps * page_bytes);
-  return S < 2 ? 2 : (S > 4 ? 4 : S);
+  int S = (48 * 1024) / (kWarps * page_bytes);
+  S = S < 2 ? 2 : (S > 4 ? 4 : S);
+  while (S > 0 && kWarps * S * (page_bytes + 8) > 227 * 1024) --S;
+  return S;
 }
 }  // namespace
 
 bool attend_mma_tq(const oscar_ctx& c) { return OSCAR_TQ && c.bits == 2 && pick_tq(c.g, c.ng) != nullptr; }
 
 bool attend_mma_supported(const oscar_ctx& c) {
-  return c.d == 128 && pick(c.bits, c.g, c.ng) != nullptr && c.P % 16 == 0;
+  return c.d == 128 && pick(c.bits, c.g, c.ng) != nullptr && c.P % 16 == 0 && stages_for(c.page_bytes) > 0;
 }
 
 int attend_mma_total_warps(const oscar_ctx& c) {

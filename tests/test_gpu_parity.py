@@ -145,6 +145,29 @@ def test_quantize_append_parity(bits, G, rho, variant, Tn, slot_mode):
             assert np.abs(g_ - r_).max() <= step, (name, h)
 
 
+@pytest.mark.parametrize("P,bits,G", [(16, 2, 64), (256, 2, 128), (32, 4, 32), (128, 4, 64)])
+def test_quantize_append_page_sizes(P, bits, G):
+    """Other page sizes through the default (tensor-core where supported) append: 700 tokens in
+    consecutive slots from a 16-aligned start (staged V path) plus random slots."""
+    torch = _torch()
+    rng = np.random.default_rng(P + bits * 10 + G)
+    H, Tn = 4, 1000
+    npages = (2000 + P - 1) // P
+    fmt = O.PageFormat(128, bits, G, P)
+    K, V = synth.gen_keys(rng, Tn, H, 128), synth.gen_values(rng, Tn, H, 128)
+    RK, RV = synth.gen_rotation(rng, H, 128), synth.gen_rotation(rng, H, 128)
+    run = np.arange(208, 908)
+    rest = np.setdiff1d(np.arange(npages * P), run)
+    slots = np.concatenate([run, rng.permutation(rest)[:Tn - 700]]).astype(np.int64)
+    ref = np.zeros((npages, H, fmt.page_bytes), np.uint8)
+    O.quantize_append(K, V, slots, RK, RV, fmt, ref)
+    o = make(num_q_heads=H * 4, num_kv_heads=H, bits=bits, group_size=G, page_size=P)
+    pool = torch.zeros((npages, H, o.page_bytes()), dtype=torch.uint8, device="cuda")
+    o.quantize_append(T(K, torch.bfloat16), T(V, torch.bfloat16), T(slots), T(RK), T(RV), pool)
+    got = pool.cpu().numpy()
+    assert (got != ref).sum() / got.size < 2e-4
+
+
 # ---------------------------------------------------------------------------- attention
 def _oracle_pool(rng, fmt, B, Hkv, L, shuffle=True):
     max_pages = (max(L) + fmt.P - 1) // fmt.P if len(L) else 1
@@ -209,6 +232,23 @@ def test_attend_parity(cfg, variant, pps):
     assert np.array_equal(np.isfinite(lg), fin)
     # lse: the IMMA path quantizes q̃ to 15 bits (reading Z31): logit error <= ~1e-4 relative
     assert (np.abs(lg[fin] - ref_lse[fin]) <= 1e-3 + 1e-4 * np.abs(ref_lse[fin])).all()
+
+
+@pytest.mark.parametrize("P,bits,G,Hq,Hkv", [(32, 2, 64, 32, 8), (128, 2, 64, 32, 8), (16, 2, 128, 16, 2),
+                                            (256, 4, 64, 8, 2), (32, 4, 32, 8, 2)])
+def test_attend_page_sizes(P, bits, G, Hq, Hkv):
+    """Page sizes other than 64 (the FULL-page fast path never applies): tensor-core kernels'
+    generic masked path against the oracle, ragged lengths."""
+    torch = _torch()
+    rng = np.random.default_rng(P * 7 + bits + G)
+    fmt = O.PageFormat(128, bits, G, P)
+    L = [5 * P + 3, P, 1]
+    pt, pool, RK, RV = _oracle_pool(rng, fmt, len(L), Hkv, L)
+    q = synth.gen_decode_q(rng, len(L), Hq, 128)
+    ref, _ = O.attend(q, pt, L, pool, RK, RV, fmt, Hkv)
+    o = make(num_q_heads=Hq, num_kv_heads=Hkv, bits=bits, group_size=G, page_size=P)
+    out32, out16, _ = _run_attend(o, q, pt, L, pool, RK, RV)
+    assert np.abs(out32.cpu().numpy().astype(np.float64) - ref).max() <= 2e-3
 
 
 def test_attend_page_indirection_invariance():

@@ -110,6 +110,7 @@ struct TcParams {
   uint8_t* pool;
   int hkv, P, page_bytes, row_bytes, vcodes_off, meta_off, ng, G, bits;
   int cpp, tiles_per_pair;
+  int lgP;                          // log2(P) if P is a power of two, else -1
 };
 
 // Σ_i 0x4B400000 << (BITS·i) mod 2^32 over the codes of one 32-bit word: the constant part of
@@ -257,8 +258,10 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
       const bool fastV = isV && __all_sync(0xffffffffu, valid && slot == slot0 + lane && (slot0 & 15) == 0);
       // (G = 128: rows past T still take part in the partner exchange below; they store nothing)
       if (!valid && G != 128) continue;
-      const int64_t page = valid ? slot / p.P : 0;
-      const int u = valid ? (int)(slot % p.P) : 0;
+      // (page, offset) of the slot: shift / mask when P is a power of two (the 64-bit division
+      // costs ~40 instructions per row)
+      const int64_t page = !valid ? 0 : (p.lgP >= 0 ? (slot >> p.lgP) : slot / p.P);
+      const int u = !valid ? 0 : (p.lgP >= 0 ? (int)(slot & (p.P - 1)) : (int)(slot % p.P));
       uint8_t* blk = p.pool + (page * p.hkv + h) * (int64_t)p.page_bytes;
       // codes: the magic add leaves float bits 0x4B400000 + code; accumulate bits << shift with
       // one LEA per code and remove the constant part once per word
@@ -287,14 +290,28 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
         const __half s16 = __float2half_rn(s), m16 = __float2half_rn(mn);
         const float sf = __half2float(s16), m = __half2float(m16);
         const float inv = sf > 0.f ? __fdiv_rn(1.f, sf) : 0.f;
+        // reading Z4: rint(RN(x - m)·inv) with the exact product: one FFMA with the 1.5·2^23
+        // magic constant (round-half-even), clamp on the float bits (same exponent).  The code
+        // is monotone in x, so when the group's min and max land inside [0, q_max] no value of
+        // the group needs the clamp (the usual case: only ranges below the fp16 resolution of
+        // their offset can push an end out)
+        const int lo_b = __float_as_int(__fmaf_rn(__fsub_rn(mn, m), inv, 12582912.f));
+        const int hi_b = __float_as_int(__fmaf_rn(__fsub_rn(mx, m), inv, 12582912.f));
+        if (lo_b >= 0x4B400000 && hi_b <= 0x4B400000 + QMAX) {
 #pragma unroll
-        for (int c = 0; c < GH; ++c) {
-          // reading Z4: rint(RN(x - m)·inv) with the exact product: one FFMA with the 1.5·2^23
-          // magic constant (round-half-even), clamp on the float bits (same exponent)
-          const float tq = __fmaf_rn(__fsub_rn(__uint_as_float(v[gi * GH + c]), m), inv, 12582912.f);
-          const uint32_t bits = (uint32_t)min(max(__float_as_int(tq), 0x4B400000), 0x4B400000 + QMAX);
-          const int idx = gi * GH + c;            // code index within the half row
-          packed[idx * BITS / 32] += bits << ((idx * BITS) & 31);
+          for (int c = 0; c < GH; ++c) {
+            const float tq = __fmaf_rn(__fsub_rn(__uint_as_float(v[gi * GH + c]), m), inv, 12582912.f);
+            const int idx = gi * GH + c;          // code index within the half row
+            packed[idx * BITS / 32] += __float_as_uint(tq) << ((idx * BITS) & 31);
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < GH; ++c) {
+            const float tq = __fmaf_rn(__fsub_rn(__uint_as_float(v[gi * GH + c]), m), inv, 12582912.f);
+            const uint32_t bits = (uint32_t)min(max(__float_as_int(tq), 0x4B400000), 0x4B400000 + QMAX);
+            const int idx = gi * GH + c;
+            packed[idx * BITS / 32] += bits << ((idx * BITS) & 31);
+          }
         }
         const int grp = (half * 64 + gi * GH) / G;
         if (valid && (G < 128 || half == 0))
@@ -334,8 +351,10 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
           const int cidx = pass * 64 + tp;        // 16-B chunk within the quarter
           const int tile = cidx / RB;             // RB chunks of 16 B per 16-token tile
           const int64_t sl = slot0 + 16 * tile;
-          uint8_t* dst = p.pool + ((sl / p.P) * p.hkv + h) * (int64_t)p.page_bytes + p.vcodes_off +
-                         16 * RB * (int)((sl % p.P) >> 4) + 16 * (cidx % RB);
+          const int64_t pg = p.lgP >= 0 ? (sl >> p.lgP) : sl / p.P;
+          const int off = p.lgP >= 0 ? (int)(sl & (p.P - 1)) : (int)(sl % p.P);
+          uint8_t* dst = p.pool + (pg * p.hkv + h) * (int64_t)p.page_bytes + p.vcodes_off +
+                         16 * RB * (off >> 4) + 16 * (cidx % RB);
           uint4 q;
           asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n"
                        : "=r"(q.x), "=r"(q.y), "=r"(q.z), "=r"(q.w) : "r"(stg + tile * TILE + 16 * (cidx % RB)));
@@ -412,6 +431,9 @@ cudaError_t launch_append_tc(const oscar_ctx& c, const void* K, const void* V, c
   p.slots = slots; p.T = T; p.RK = RK; p.RV = RV; p.pool = static_cast<uint8_t*>(pool);
   p.hkv = c.hkv; p.P = c.P; p.page_bytes = c.page_bytes; p.row_bytes = c.row_bytes;
   p.vcodes_off = c.vcodes_off; p.meta_off = c.meta_off; p.ng = c.ng; p.G = c.G; p.bits = c.bits;
+  p.lgP = -1;
+  for (int k = 0; k < 16; ++k)
+    if ((1 << k) == c.P) p.lgP = k;
   const int pairs = 2 * c.hkv;
   p.tiles_per_pair = (int)((T + kTok - 1) / kTok);
   int cpp = c.num_sms / pairs;

@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(256) attend_merge_kernel(AttnParams p, const f
                                                            void* __restrict__ out, int out_fp32,
                                                            float* __restrict__ lse) {
   constexpr int WPH = 8 / GQ;                        // warps per query head
-  constexpr int NB = 16;                             // splits per load batch per warp
+  constexpr int NB = 8;                              // splits per load batch (two in flight) per warp
   constexpr int HPT = (GQ + 1) / 2;                  // heads per thread in the un-rotation
   extern __shared__ __align__(128) float Rs[];       // [128][128] R_V[h]
   __shared__ __align__(16) float po[8][kD];
@@ -379,9 +379,9 @@ __global__ void __launch_bounds__(256) attend_merge_kernel(AttnParams p, const f
     auto prow = [&](int s) -> size_t { return rbh * ns + s; };
     float mw = -INFINITY, Lw = 0.f;
     float4 ow = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int s0 = part; s0 < ns; s0 += WPH * NB) {
-      float4 x[NB];
-      float ms[NB], ls[NB];
+    // software-pipelined fold: the loads of the next batch of NB splits are in flight while
+    // the current batch is folded (running max; empty splits have m = -inf and weight 0)
+    auto load = [&](int s0, float4 (&x)[NB], float (&ms)[NB], float (&ls)[NB]) {
 #pragma unroll
       for (int k = 0; k < NB; ++k) {
         const int s = s0 + k * WPH;
@@ -392,6 +392,8 @@ __global__ void __launch_bounds__(256) attend_merge_kernel(AttnParams p, const f
         ms[k] = ok ? __ldcg(p.ws_m + r) : -INFINITY;
         ls[k] = ok ? __ldcg(p.ws_l + r) : 0.f;
       }
+    };
+    auto fold = [&](float4 (&x)[NB], float (&ms)[NB], float (&ls)[NB]) {
       float nm = mw;
 #pragma unroll
       for (int k = 0; k < NB; ++k) nm = fmaxf(nm, ms[k]);
@@ -401,15 +403,22 @@ __global__ void __launch_bounds__(256) attend_merge_kernel(AttnParams p, const f
 #pragma unroll
       for (int k = 0; k < NB; ++k) {
         const float wt = ms[k] == -INFINITY ? 0.f : exp2f(ms[k] - nm);   // 0 for empty splits
-        if (ms[k] == -INFINITY) {                  // (their õ and l are never written)
-          x[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-          ls[k] = 0.f;
-        }
         ow.x = fmaf(x[k].x, wt, ow.x); ow.y = fmaf(x[k].y, wt, ow.y);
         ow.z = fmaf(x[k].z, wt, ow.z); ow.w = fmaf(x[k].w, wt, ow.w);
         Lw = fmaf(ls[k], wt, Lw);
       }
       mw = nm;
+    };
+    float4 xa[NB], xb[NB];
+    float ma[NB], mb[NB], la[NB], lb[NB];
+    constexpr int STEP = WPH * NB;
+    load(part, xa, ma, la);
+    for (int s0 = part; s0 < ns; s0 += 2 * STEP) {
+      if (s0 + STEP < ns) load(s0 + STEP, xb, mb, lb);
+      fold(xa, ma, la);
+      if (s0 + STEP >= ns) break;
+      if (s0 + 2 * STEP < ns) load(s0 + 2 * STEP, xa, ma, la);
+      fold(xb, mb, lb);
     }
     reinterpret_cast<float4*>(po[w])[lane] = ow;
     if (lane == 0) { pm[w] = mw; pl[w] = Lw; }

@@ -13,7 +13,7 @@
 //               (reading Z4: one FFMA + bit clamp per code), pack, store into the slot's page
 //               block (FORMAT, common.cuh); V codes of whole 16-token tiles are staged in smem in
 //               FORMAT order and written as 16-B chunks.
-// Scope of this kernel: b in {2, 4}, G in {32, 64, 128} (a G = 128 group spans the two channel
+// Scope of this kernel: b in {2, 3, 4}, G in {32, 64, 128} (a G = 128 group spans the two channel
 // halves: the two warps swap min/max through smem), no clipping; other configs use the simple
 // kernel (append.cu).
 #include <cuda.h>
@@ -265,9 +265,21 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
       uint8_t* blk = p.pool + (page * p.hkv + h) * (int64_t)p.page_bytes;
       // codes: the magic add leaves float bits 0x4B400000 + code; accumulate bits << shift with
       // one LEA per code and remove the constant part once per word
+      // (3-bit codes straddle words: the code is taken out of the float bits and OR-ed in,
+      // its high bits spilling into the next word)
       uint32_t packed[BITS * 2];
 #pragma unroll
-      for (int w = 0; w < BITS * 2; ++w) packed[w] = 0u - magic_words<BITS>();
+      for (int w = 0; w < BITS * 2; ++w) packed[w] = BITS == 3 ? 0u : 0u - magic_words<BITS>();
+      auto put = [&](int idx, uint32_t fbits) {
+        const int bit = idx * BITS, wd = bit >> 5, sh = bit & 31;
+        if (BITS == 3) {
+          const uint32_t code = fbits - 0x4B400000u;
+          packed[wd] |= code << sh;
+          if (sh > 29) packed[wd + 1] |= code >> (32 - sh);
+        } else {
+          packed[wd] += fbits << sh;
+        }
+      };
 #pragma unroll
       for (int gi = 0; gi < GPH; ++gi) {
         float mn = __uint_as_float(v[gi * GH]), mx = mn;
@@ -301,16 +313,14 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
 #pragma unroll
           for (int c = 0; c < GH; ++c) {
             const float tq = __fmaf_rn(__fsub_rn(__uint_as_float(v[gi * GH + c]), m), inv, 12582912.f);
-            const int idx = gi * GH + c;          // code index within the half row
-            packed[idx * BITS / 32] += __float_as_uint(tq) << ((idx * BITS) & 31);
+            put(gi * GH + c, __float_as_uint(tq));   // code index within the half row
           }
         } else {
 #pragma unroll
           for (int c = 0; c < GH; ++c) {
             const float tq = __fmaf_rn(__fsub_rn(__uint_as_float(v[gi * GH + c]), m), inv, 12582912.f);
             const uint32_t bits = (uint32_t)min(max(__float_as_int(tq), 0x4B400000), 0x4B400000 + QMAX);
-            const int idx = gi * GH + c;
-            packed[idx * BITS / 32] += bits << ((idx * BITS) & 31);
+            put(gi * GH + c, bits);
           }
         }
         const int grp = (half * 64 + gi * GH) / G;
@@ -323,16 +333,22 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
       constexpr int RB = 16 * BITS;               // bytes of a row
       if (!isV) {
         uint8_t* dst = blk + fmt_krow(u) * p.row_bytes + half * HB;
+        if (HB % 16 == 0) {
 #pragma unroll
-        for (int w4 = 0; w4 < BITS / 2; ++w4)
-          *reinterpret_cast<uint4*>(dst + 16 * w4) =
-              make_uint4(packed[4 * w4], packed[4 * w4 + 1], packed[4 * w4 + 2], packed[4 * w4 + 3]);
+          for (int w4 = 0; w4 < HB / 16; ++w4)
+            *reinterpret_cast<uint4*>(dst + 16 * w4) =
+                make_uint4(packed[4 * w4], packed[4 * w4 + 1], packed[4 * w4 + 2], packed[4 * w4 + 3]);
+        } else {                                  // 3-bit: 24-B half rows, 8-B aligned
+#pragma unroll
+          for (int w2 = 0; w2 < HB / 8; ++w2)
+            *reinterpret_cast<uint2*>(dst + 8 * w2) = make_uint2(packed[2 * w2], packed[2 * w2 + 1]);
+        }
       } else if (fastV) {
         constexpr int TILE = 16 * RB + 16;        // staged 16-token tile (+16 B: bank shift)
         const uint32_t stg = su32(S.vstage[par][quarter]);
-        // this token's bytes at their FORMAT offsets inside its 16-token tile (fmt_vbyte with
-        // u = lane % 16: compile-time part per byte + 16·(4-token group) + token-in-group)
-        const uint32_t base = stg + (lane >> 4) * TILE + 16 * ((lane >> 2) & 3) + (lane & 3);
+        // this token's bytes at their FORMAT offsets inside its 16-token tile (fmt_vbyte is
+        // additive: the token part fmt_vbyte(u, 0) + the compile-time byte part fmt_vbyte(0, j))
+        const uint32_t base = stg + (lane >> 4) * TILE + fmt_vbyte(lane & 15, 0, RB);
         auto put = [&](auto half_c) {
           constexpr int H = decltype(half_c)::value;
 #pragma unroll
@@ -347,8 +363,9 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
         // copy out: 2 tiles x 16·RB bytes, 16 B per thread per pass (64 threads)
         const int tp = half * 32 + lane;
 #pragma unroll
-        for (int pass = 0; pass < (2 * 16 * RB) / (16 * 64); ++pass) {
+        for (int pass = 0; pass < (2 * RB + 63) / 64; ++pass) {
           const int cidx = pass * 64 + tp;        // 16-B chunk within the quarter
+          if (cidx >= 2 * RB) break;              // (3-bit: 96 chunks)
           const int tile = cidx / RB;             // RB chunks of 16 B per 16-token tile
           const int64_t sl = slot0 + 16 * tile;
           const int64_t pg = p.lgP >= 0 ? (sl >> p.lgP) : sl / p.P;
@@ -410,6 +427,9 @@ TcFn pick(int bits, int G) {
   if (bits == 4 && G == 64) return append_tc_kernel<4, 64>;
   if (bits == 4 && G == 32) return append_tc_kernel<4, 32>;
   if (bits == 2 && G == 128) return append_tc_kernel<2, 128>;
+  if (bits == 3 && G == 32) return append_tc_kernel<3, 32>;
+  if (bits == 3 && G == 64) return append_tc_kernel<3, 64>;
+  if (bits == 3 && G == 128) return append_tc_kernel<3, 128>;
   if (bits == 4 && G == 128) return append_tc_kernel<4, 128>;
   return nullptr;
 }

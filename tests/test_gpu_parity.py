@@ -115,6 +115,8 @@ def _slots(rng, mode, Tn, npages):
     (3, 128, (1.0, 1.0), 0, 40, "perm"),
     (2, 32, (1.0, 1.0), 0, 1000, "contig200"), (4, 32, (1.0, 1.0), 0, 1280, "contig0"),
     (2, 128, (1.0, 1.0), 0, 1000, "contig208"), (4, 128, (1.0, 1.0), 0, 1000, "perm"),   # G = 128 on tcgen05
+    (3, 64, (1.0, 1.0), 0, 1000, "contig208"), (3, 128, (1.0, 1.0), 0, 1000, "perm"),    # 3-bit on tcgen05
+    (3, 32, (1.0, 1.0), 0, 1000, "contig200"),
 ])
 def test_quantize_append_parity(bits, G, rho, variant, Tn, slot_mode):
     torch = _torch()

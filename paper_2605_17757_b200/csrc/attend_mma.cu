@@ -190,6 +190,12 @@ attend_partial_mma(AttnParams p, int S) {
   constexpr int NTQ = (GQ + 3) / 4;           // TQ: QK N-tiles of 4 heads x (hi|lo)
   constexpr int NC = GQ * NG;                 // (group, head) combos
   constexpr int NT = (NC + 7) / 8;            // 8-combo tiles (QK M-tiles / PV N-tiles)
+  // PVG (TQ, g = 8, two groups): PV M-tiles are group-pure (rows gid / gid + 8 take V words
+  // 2p / 2p + 1 = channels 64p + 4·gid + q and + 32), so each multiplies only the 8 head
+  // columns of its own group: one N-tile instead of two, half the PV HMMAs and accumulators
+  constexpr bool PVG = TQ && GQ == 8 && NG == 2;
+  constexpr int NTA = PVG ? 1 : NT;           // PV accumulator N-tiles
+  constexpr int NBS = PVG ? NG : NT;          // PV B-operand sets (per group, or per N-tile)
   constexpr int kChunk = NT > 1 ? OSCAR_CHUNK_NT2 : OSCAR_CHUNK;   // 16-token sub-tiles per softmax chunk
   constexpr int RB = 16 * BITS;               // packed row bytes (d = 128)
   constexpr int G = 128 / NG;
@@ -314,18 +320,19 @@ attend_partial_mma(AttnParams p, int S) {
         for (int g = 0; g < NG; ++g) qs_h[jt][g] = hq < GQ ? (float)p.qsum[row * 8 + g] * kBScale : 0.f;
       }
     }
-    float acc[8][NT][4];
+    float acc[8][NTA][4];
     f2 mv2[NT];                               // Σ p·m_V of this lane's combo over its tokens (2 partial sums)
-    float accm[TQ ? NT : 1][4];               // TQ: Σ p·m_V through the tensor core (rows all equal)
+    float accm[TQ ? NBS : 1][4];              // TQ: Σ p·m_V through the tensor core (rows all equal)
 #pragma unroll
-    for (int j = 0; j < NT; ++j) {
-      mv2[j] = f2{0.f, 0.f};
+    for (int j = 0; j < NT; ++j) mv2[j] = f2{0.f, 0.f};
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        if constexpr (TQ) accm[j][e] = 0.f;
+    for (int e = 0; e < 4; ++e) {
+#pragma unroll
+      for (int j = 0; j < (TQ ? NBS : 1); ++j) accm[j][e] = 0.f;
+#pragma unroll
+      for (int j = 0; j < NTA; ++j)
 #pragma unroll
         for (int i = 0; i < 8; ++i) acc[i][j][e] = 0.f;
-      }
     }
     // scores are kept relative to m_run (log2 domain); m_run starts at 0 and the first chunk
     // of the item moves it to that chunk's max, later chunks only when the max grows
@@ -620,18 +627,21 @@ attend_partial_mma(AttnParams p, int S) {
           // accumulator column (combo 8j + 2t + e) of head (8j + 2t + e) % GQ: its alpha lives
           // in lane t' = head % 4, slot head / 4
 #pragma unroll
-          for (int j = 0; j < NT; ++j)
+          for (int j = 0; j < NBS; ++j)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-              const int hq = (8 * j + 2 * t + e) % GQ;
+              // PVG: every set's column 2t + e is head 2t + e
+              const int hq = PVG ? 2 * t + e : (8 * j + 2 * t + e) % GQ;
               float a = __shfl_sync(0xffffffffu, alpha[0], hq & 3);
               if (NTQ > 1) {
                 const float a1 = __shfl_sync(0xffffffffu, alpha[NTQ - 1], hq & 3);
                 a = hq >= 4 ? a1 : a;
               }
               accm[j][e] *= a; accm[j][e + 2] *= a;
+              if (j < NTA) {
 #pragma unroll
-              for (int i = 0; i < 8; ++i) { acc[i][j][e] *= a; acc[i][j][e + 2] *= a; }
+                for (int i = 0; i < 8; ++i) { acc[i][j][e] *= a; acc[i][j][e + 2] *= a; }
+              }
             }
         }
         // ---- PV per sub-tile
@@ -655,10 +665,10 @@ attend_partial_mma(AttnParams p, int S) {
             if (hc >= 4) { X = X1; Y = Y1; }
           }
           const uint32_t p02 = __byte_perm(X, Y, 0x5410), p13 = __byte_perm(X, Y, 0x7632);
-          uint32_t bpv[NT][2];
+          uint32_t bpv[NBS][2];
 #pragma unroll
-          for (int j = 0; j < NT; ++j) {
-            const int gc = min((8 * j + gid) / GQ, NG - 1);
+          for (int j = 0; j < NBS; ++j) {
+            const int gc = PVG ? j : min((8 * j + gid) / GQ, NG - 1);
             const uint4 mv4 = *reinterpret_cast<const uint4*>(meta + 128 * NG * st + 128 * gc + 32 * t + 16);
             uint32_t mw[4] = {mv4.x, mv4.y, mv4.z, mv4.w};
             if (!FULL) {   // masked tokens may carry garbage metadata: keep them out
@@ -689,12 +699,21 @@ attend_partial_mma(AttnParams p, int S) {
             const int q = i % CPB;
             const uint32_t msk = kCodeMask << (BITS * q);
             uint32_t a[4];
-            a[0] = vw[i / CPB] & msk;
-            a[1] = vw[VW / 2 + i / CPB] & msk;
-            a[2] = vs[i / CPB] & msk;
-            a[3] = vs[VW / 2 + i / CPB] & msk;
+            if constexpr (PVG) {               // M-tile i: group p = i / CPB, words 2p / 2p + 1
+              const int pg2 = 2 * (i / CPB);
+              a[0] = vw[pg2] & msk;
+              a[1] = vw[pg2 + 1] & msk;
+              a[2] = vs[pg2] & msk;
+              a[3] = vs[pg2 + 1] & msk;
+              hmma16816(acc[i][0], a, bpv[i / CPB][0], bpv[i / CPB][1]);
+            } else {
+              a[0] = vw[i / CPB] & msk;
+              a[1] = vw[VW / 2 + i / CPB] & msk;
+              a[2] = vs[i / CPB] & msk;
+              a[3] = vs[VW / 2 + i / CPB] & msk;
 #pragma unroll
-            for (int j = 0; j < NT; ++j) hmma16816(acc[i][j], a, bpv[j][0], bpv[j][1]);
+              for (int j = 0; j < NTA; ++j) hmma16816(acc[i][j], a, bpv[j][0], bpv[j][1]);
+            }
           }
         }
       }
@@ -737,13 +756,27 @@ attend_partial_mma(AttnParams p, int S) {
       mv_acc[j] += __shfl_xor_sync(0xffffffffu, mv_acc[j], 2);
     }
     const size_t row0 = ((size_t)I.b * p.hq + (size_t)I.h * GQ) * p.n_splits + I.split;
+    if constexpr (PVG) {
+      // M-tile i = group p = i / CPB; rows gid / gid + 8 = channels 64p + CPB·gid + q (+ 32)
 #pragma unroll
-    for (int j = 0; j < NT; ++j)
+      for (int e = 0; e < 4; ++e) {
+        const int head = 2 * t + (e & 1);
+        const size_t row = row0 + (size_t)head * p.n_splits;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float unscale = (float)(1 << (24 - BITS * (i % CPB)));
+          const int ch = 64 * (i / CPB) + CPB * gid + (i % CPB) + ((e >> 1) ? 32 : 0);
+          p.ws_o[row * 128 + ch] = fmaf(acc[i][0][e], unscale, accm[i / CPB][e & 1]);
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < (PVG ? 0 : NT); ++j)
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int col = 2 * t + (e & 1);
         const int cc = 8 * j + col;
-        const float mvs = TQ ? accm[j][e & 1]                               // this lane's column
+        const float mvs = TQ ? accm[j % NBS][e & 1]                         // this lane's column
                              : __shfl_sync(0xffffffffu, mv_acc[j], 4 * col);   // combo col = gid of lane 4·col
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -751,7 +784,7 @@ attend_partial_mma(AttnParams p, int S) {
           const int ch = pv_channel<BITS>(i, gid, e >> 1);
           if (cc < NC && ch / G == cc / GQ) {
             const size_t row = row0 + (size_t)(cc % GQ) * p.n_splits;
-            p.ws_o[row * 128 + ch] = fmaf(acc[i][j][e], unscale, mvs);
+            p.ws_o[row * 128 + ch] = fmaf(acc[i][j % NTA][e], unscale, mvs);
           }
         }
       }

@@ -324,15 +324,16 @@ attend_partial_mma(AttnParams p, int S) {
     f2 mv2[NT];                               // Σ p·m_V of this lane's combo over its tokens (2 partial sums)
     float accm[TQ ? NBS : 1][4];              // TQ: Σ p·m_V through the tensor core (rows all equal)
 #pragma unroll
-    for (int j = 0; j < NT; ++j) mv2[j] = f2{0.f, 0.f};
+    for (int j = 0; j < NT; ++j) {
+      mv2[j] = f2{0.f, 0.f};
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
+      for (int e = 0; e < 4; ++e) {
+        if (TQ && j < NBS) accm[j][e] = 0.f;
+        if (j < NTA) {
 #pragma unroll
-      for (int j = 0; j < (TQ ? NBS : 1); ++j) accm[j][e] = 0.f;
-#pragma unroll
-      for (int j = 0; j < NTA; ++j)
-#pragma unroll
-        for (int i = 0; i < 8; ++i) acc[i][j][e] = 0.f;
+          for (int i = 0; i < 8; ++i) acc[i][j][e] = 0.f;
+        }
+      }
     }
     // scores are kept relative to m_run (log2 domain); m_run starts at 0 and the first chunk
     // of the item moves it to that chunk's max, later chunks only when the max grows

@@ -298,6 +298,33 @@ def test_attend_full_size_sampled():
         assert np.abs(got[b] - ref[0]).max() <= 2e-3
 
 
+def test_attend_c4_full_size_sampled():
+    """C4 at full size (g = 8: 64 q / 8 kv heads, 2-bit, G = 64, B = 16, L = 131072) in the
+    bench's launch configuration on a random packed pool; one sequence (all 64 heads) against
+    the oracle."""
+    torch = _torch()
+    B, L, Hq, Hkv, P = 16, 131072, 64, 8, 64
+    o = make(num_q_heads=Hq, num_kv_heads=Hkv, bits=2, group_size=64)
+    fmt = O.PageFormat(128, 2, 64, P)
+    max_pages = L // P
+    gen = torch.Generator(device="cuda").manual_seed(2)
+    pool = synth.torch_random_pool(gen, B * max_pages, Hkv, o.page_bytes(), fmt.meta_off, P * 2, "cuda")
+    rng = np.random.default_rng(2)
+    pt = synth.contiguous_page_table(B, max_pages, shuffle_rng=rng)
+    RK, RV = synth.gen_rotation(rng, Hkv, 128), synth.gen_rotation(rng, Hkv, 128)
+    q = synth.gen_decode_q(rng, B, Hq, 128)
+    seq = np.full(B, L, np.int32)
+    seq[3] = L - 5000
+    ws = torch.empty(o.attend_workspace_bytes(B, max_pages), dtype=torch.uint8, device="cuda")
+    out = torch.empty((B, Hq, 128), dtype=torch.float32, device="cuda")
+    o.attend(T(q, torch.bfloat16), T(pt), T(seq), pool, T(RK), T(RV), ws, out)
+    got = out.cpu().numpy()
+    b = 3
+    sub = pool[torch.from_numpy(pt[b].astype(np.int64)).cuda()].cpu().numpy()
+    ref, _ = O.attend(q[b:b + 1], np.arange(max_pages, dtype=np.int32)[None], [seq[b]], sub, RK, RV, fmt, Hkv)
+    assert np.abs(got[b] - ref[0]).max() <= 2e-3
+
+
 # ---------------------------------------------------------------------------- calibration
 @pytest.mark.parametrize("variant,N,Hq,Hkv", [(0, 3000, 8, 2), (1, 3000, 8, 2), (0, 2500, 16, 2), (0, 9000, 2, 2)])
 def test_calibration_parity_by_invariants(variant, N, Hq, Hkv):

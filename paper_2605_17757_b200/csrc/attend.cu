@@ -175,7 +175,10 @@ __global__ void __launch_bounds__(512) attend_prologue_kernel(PrologueParams pp)
       const int hd = 4 * jt + (gid >> 1), lo = gid & 1;
       uint32_t v = 0;
       if (hd < GQ) {
-        const int j = (kk >> 1) ? 4 + t : t, sft = 2 * (kk & 1) + r;
+        // G = 32: k-slot 4t + i + 16r of k-step kk <-> field t of byte i of word 2kk + r
+        const bool g32 = pp.lgG == 5;
+        const int j = g32 ? 2 * kk + r : ((kk >> 1) ? 4 + t : t);
+        const int sft = g32 ? t : 2 * (kk & 1) + r;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int qv = qis[hd][16 * j + 4 * i + sft];

@@ -186,16 +186,19 @@ __device__ __forceinline__ Item decode_item(const AttnParams& p, int it) {
 template <int BITS, int GQ, int NG, bool TQ>
 __global__ void __launch_bounds__(kWarps * 32, (GQ * NG <= 8 ? OSCAR_MINB : OSCAR_MINB_NT2))
 attend_partial_mma(AttnParams p, int S) {
-  static_assert(!TQ || (BITS == 2 && NG <= 2 && GQ >= 2), "token-row QK layout: 2-bit, G >= 64, g >= 2");
+  static_assert(!TQ || (BITS == 2 && GQ >= 2 && (NG <= 2 || (NG == 4 && GQ == 4))),
+                "token-row QK layout: 2-bit, g >= 2 (G = 32: g = 4)");
   constexpr int NTQ = (GQ + 3) / 4;           // TQ: QK N-tiles of 4 heads x (hi|lo)
   constexpr int NC = GQ * NG;                 // (group, head) combos
   constexpr int NT = (NC + 7) / 8;            // 8-combo tiles (QK M-tiles / PV N-tiles)
   // PVG (TQ, g = 8, two groups): PV M-tiles are group-pure (rows gid / gid + 8 take V words
   // 2p / 2p + 1 = channels 64p + 4·gid + q and + 32), so each multiplies only the 8 head
   // columns of its own group: one N-tile instead of two, half the PV HMMAs and accumulators
-  constexpr bool PVG = TQ && GQ == 8 && NG == 2;
+  // G = 32, g = 4 (PVG too): M-tile pair p takes V words 2p (rows gid: group 2p) / 2p + 1 (rows
+  // gid + 8: group 2p + 1); its 8 columns are the 4 heads of group 2p, then of group 2p + 1
+  constexpr bool PVG = TQ && ((GQ == 8 && NG == 2) || (GQ == 4 && NG == 4));
   constexpr int NTA = PVG ? 1 : NT;           // PV accumulator N-tiles
-  constexpr int NBS = PVG ? NG : NT;          // PV B-operand sets (per group, or per N-tile)
+  constexpr int NBS = PVG ? 2 : NT;           // PV B-operand sets (per M-tile pair, or per N-tile)
   constexpr int kChunk = NT > 1 ? OSCAR_CHUNK_NT2 : OSCAR_CHUNK;   // 16-token sub-tiles per softmax chunk
   constexpr int RB = 16 * BITS;               // packed row bytes (d = 128)
   constexpr int G = 128 / NG;
@@ -551,8 +554,18 @@ attend_partial_mma(AttnParams p, int S) {
           }
           // one ldmatrix.x4: matrices (rows 0-7 | 8-15) x (bytes 0-15 | 16-31) of the K tile, so
           // lane (gid, t) receives words t and 4 + t of rows gid and gid + 8
-          uint32_t wa[2], wb[2];
-          {
+          uint32_t wa[NG == 4 ? 8 : 2], wb[NG == 4 ? 8 : 2];
+          if constexpr (NG == 4) {
+            // G = 32: lane t takes 2-bit field t of every word of rows gid / gid + 8 (k-step g =
+            // words 2g, 2g + 1 = group g)
+            const uint4* ra = reinterpret_cast<const uint4*>(pg + (size_t)(16 * st + gid) * RB);
+            const uint4* rb = reinterpret_cast<const uint4*>(pg + (size_t)(16 * st + 8 + gid) * RB);
+            const uint4 a0 = ra[0], a1 = ra[1], b0 = rb[0], b1 = rb[1];
+            wa[0] = a0.x; wa[1] = a0.y; wa[2] = a0.z; wa[3] = a0.w;
+            wa[4] = a1.x; wa[5] = a1.y; wa[6] = a1.z; wa[7] = a1.w;
+            wb[0] = b0.x; wb[1] = b0.y; wb[2] = b0.z; wb[3] = b0.w;
+            wb[4] = b1.x; wb[5] = b1.y; wb[6] = b1.z; wb[7] = b1.w;
+          } else {
             const int mi = lane >> 3;
             const uint32_t addr = smem_u32(pg + (size_t)(16 * st + 8 * (mi >> 1) + (lane & 7)) * RB + 16 * (mi & 1));
             asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];\n"
@@ -568,15 +581,24 @@ attend_partial_mma(AttnParams p, int S) {
               for (int e = 0; e < 4; ++e) cq[jt][g][e] = 0;
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
-            // k-step kk: word kk/2 (group kk/2 when G = 64), 2-bit fields 2(kk&1) (a0, a1) and
-            // 2(kk&1)+1 (a2, a3) moved to the top of each byte (c·64, folded into qscale)
-            const int wi = kk >> 1, s0 = 6 - 4 * (kk & 1);
             uint32_t a[4];
-            a[0] = (wa[wi] << s0) & 0xC0C0C0C0u;
-            a[1] = (wb[wi] << s0) & 0xC0C0C0C0u;
-            a[2] = (wa[wi] << (s0 - 2)) & 0xC0C0C0C0u;
-            a[3] = (wb[wi] << (s0 - 2)) & 0xC0C0C0C0u;
-            const int g = NG == 2 ? (kk >> 1) : 0;
+            if constexpr (NG == 4) {
+              // k-step kk = group kk: field t of words 2kk (a0, a1) and 2kk + 1 (a2, a3)
+              const uint32_t mul = 1u << (6 - 2 * t);
+              a[0] = (wa[2 * kk] * mul) & 0xC0C0C0C0u;
+              a[1] = (wb[2 * kk] * mul) & 0xC0C0C0C0u;
+              a[2] = (wa[2 * kk + 1] * mul) & 0xC0C0C0C0u;
+              a[3] = (wb[2 * kk + 1] * mul) & 0xC0C0C0C0u;
+            } else {
+              // k-step kk: word kk/2 (group kk/2 when G = 64), 2-bit fields 2(kk&1) (a0, a1) and
+              // 2(kk&1)+1 (a2, a3) moved to the top of each byte (c·64, folded into qscale)
+              const int wi = kk >> 1, s0 = 6 - 4 * (kk & 1);
+              a[0] = (wa[wi] << s0) & 0xC0C0C0C0u;
+              a[1] = (wb[wi] << s0) & 0xC0C0C0C0u;
+              a[2] = (wa[wi] << (s0 - 2)) & 0xC0C0C0C0u;
+              a[3] = (wb[wi] << (s0 - 2)) & 0xC0C0C0C0u;
+            }
+            const int g = NG == 4 ? kk : (NG == 2 ? (kk >> 1) : 0);
 #pragma unroll
             for (int jt = 0; jt < NTQ; ++jt) imma16832_us(cq[jt][g], a, bq[jt][kk][0], bq[jt][kk][1]);
           }
@@ -632,7 +654,7 @@ attend_partial_mma(AttnParams p, int S) {
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
               // PVG: every set's column 2t + e is head 2t + e
-              const int hq = PVG ? 2 * t + e : (8 * j + 2 * t + e) % GQ;
+              const int hq = PVG ? (2 * t + e) % GQ : (8 * j + 2 * t + e) % GQ;
               float a = __shfl_sync(0xffffffffu, alpha[0], hq & 3);
               if (NTQ > 1) {
                 const float a1 = __shfl_sync(0xffffffffu, alpha[NTQ - 1], hq & 3);
@@ -669,7 +691,8 @@ attend_partial_mma(AttnParams p, int S) {
           uint32_t bpv[NBS][2];
 #pragma unroll
           for (int j = 0; j < NBS; ++j) {
-            const int gc = PVG ? j : min((8 * j + gid) / GQ, NG - 1);
+            // PVG: set j = M-tile pair j; column gid -> group j (g = 8) or 2j + gid / 4 (G = 32)
+            const int gc = PVG ? (NG == 4 ? 2 * j + (gid >> 2) : j) : min((8 * j + gid) / GQ, NG - 1);
             const uint4 mv4 = *reinterpret_cast<const uint4*>(meta + 128 * NG * st + 128 * gc + 32 * t + 16);
             uint32_t mw[4] = {mv4.x, mv4.y, mv4.z, mv4.w};
             if (!FULL) {   // masked tokens may carry garbage metadata: keep them out
@@ -758,15 +781,20 @@ attend_partial_mma(AttnParams p, int S) {
     }
     const size_t row0 = ((size_t)I.b * p.hq + (size_t)I.h * GQ) * p.n_splits + I.split;
     if constexpr (PVG) {
-      // M-tile i = group p = i / CPB; rows gid / gid + 8 = channels 64p + CPB·gid + q (+ 32)
+      // M-tile pair p = i / CPB; rows gid / gid + 8 = channels 64p + CPB·gid + q (+ 32).  g = 8:
+      // column = head, both row halves valid; G = 32: columns 0-3 (heads of group 2p) pair with
+      // the rows gid, columns 4-7 (group 2p + 1) with the rows gid + 8
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const int head = 2 * t + (e & 1);
+        const int col = 2 * t + (e & 1);
+        const bool upper = (e >> 1) != 0;
+        if (NG == 4 && (col >= 4) != upper) continue;
+        const int head = col % GQ;
         const size_t row = row0 + (size_t)head * p.n_splits;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const float unscale = (float)(1 << (24 - BITS * (i % CPB)));
-          const int ch = 64 * (i / CPB) + CPB * gid + (i % CPB) + ((e >> 1) ? 32 : 0);
+          const int ch = 64 * (i / CPB) + CPB * gid + (i % CPB) + (upper ? 32 : 0);
           p.ws_o[row * 128 + ch] = fmaf(acc[i][0][e], unscale, accm[i / CPB][e & 1]);
         }
       }
@@ -830,11 +858,12 @@ KernelFn pick_g(int g, int ng) {
   return nullptr;
 }
 
-// token-row QK layout (TQ): 2-bit codes, G in {64, 128}, g in {2, 4, 8}
+// token-row QK layout (TQ): 2-bit codes, G in {64, 128} with g in {2, 4, 8}, G = 32 with g = 4
 KernelFn pick_tq(int g, int ng) {
 #define OSCAR_CASE(GQ_, NG_) \
   if (g == GQ_ && ng == NG_) return attend_partial_mma<2, GQ_, NG_, true>;
-  OSCAR_CASE(2, 1) OSCAR_CASE(2, 2) OSCAR_CASE(4, 1) OSCAR_CASE(4, 2) OSCAR_CASE(8, 1) OSCAR_CASE(8, 2)
+  OSCAR_CASE(2, 1) OSCAR_CASE(2, 2) OSCAR_CASE(4, 1) OSCAR_CASE(4, 2) OSCAR_CASE(4, 4) OSCAR_CASE(8, 1)
+  OSCAR_CASE(8, 2)
 #undef OSCAR_CASE
   return nullptr;
 }

@@ -209,6 +209,7 @@ def _run_attend(o, q, pt, L, pool, RK, RV):
     dict(name="C4small", Hq=16, Hkv=2, bits=2, G=64, B=2, L=[700, 130]),     # g=8, two 8-combo tiles
     dict(name="g4G32", Hq=8, Hkv=2, bits=4, G=32, B=2, L=[450, 64]),        # 4 groups x 4 heads
     dict(name="b3", Hq=8, Hkv=2, bits=3, G=64, B=2, L=[333, 64]),           # 3-bit: simple kernels
+    dict(name="C2G32", Hq=32, Hkv=8, bits=2, G=32, B=3, L=[1000, 77, 0]),   # token-row layout, 4 groups
 ])
 @pytest.mark.parametrize("variant", [0, 1])
 @pytest.mark.parametrize("pps", [0, 1, 3])

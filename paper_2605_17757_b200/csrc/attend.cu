@@ -568,19 +568,21 @@ int attend_mma_total_warps(const oscar_ctx& c);                              // 
 
 // Pages per split-K work item.  Tensor-core path: as few items as keep every warp of the
 // persistent grid busy — floor(warps / (B·H_kv)) splits per (sequence, kv head) — so each warp
-// gets one balanced item (≤ 32 pages: the partial kernel holds an item's page indices one per
+// gets one balanced item (≤ 64 pages: the partial kernel holds an item's page indices two per
 // lane); fewer, longer items also cut the split partials the merge reads.
 static int choose_pps(const oscar_ctx& c, int B, int max_pages) {
   const long units = (long)B * c.hkv;
   const bool mma = c.variant == 0 && attend_mma_supported(c);
-  if (c.pages_per_split > 0) return (mma && c.pages_per_split > 32) ? 32 : c.pages_per_split;
+  if (c.pages_per_split > 0) return (mma && c.pages_per_split > 64) ? 64 : c.pages_per_split;
   if (mma) {
     const long warps = attend_mma_total_warps(c);
     long splits = units > 0 ? warps / units : 1;
     if (splits < 1) splits = 1;
     long pps = (max_pages + splits - 1) / splits;
     const long lo = max_pages < 4 ? (max_pages > 0 ? max_pages : 1) : 4;
-    pps = pps < lo ? lo : (pps > 32 ? 32 : pps);
+    // one wave of items of up to 64 pages when that covers the cache; otherwise items of at most
+    // 32 pages, several per warp from the work counter (short items keep the last wave short)
+    pps = pps < lo ? lo : (pps > 64 ? 32 : pps);
     return (int)pps;
   }
   const long target = (long)c.num_sms * 8;

@@ -230,20 +230,23 @@ attend_partial_mma(AttnParams p, int S) {
   auto fetch_async = [&]() { return lane == 0 ? atomicAdd(p.work, 1) + 2 * total_warps : 0; };
   auto bcast = [&](int v) { return __shfl_sync(0xffffffffu, v, 0); };
   int cur = gw, nxt = gw + total_warps;
-  // loader view of an item: pages, kv head; lane l holds the item's page index l (pps <= 32)
-  int cur_np = 0, cur_h = 0, pidx_cur = 0, nxt_np = 0, nxt_h = 0, pidx_nxt = 0;
+  // loader view of an item: pages, kv head; lane l holds the item's page indices l and 32 + l
+  // (pps <= 64)
+  int cur_np = 0, cur_h = 0, pidx_cur = 0, pidx_cur2 = 0, nxt_np = 0, nxt_h = 0, pidx_nxt = 0, pidx_nxt2 = 0;
   int cur_last = -1, nxt_last = -1;   // local index of the sequence's last page in the item, or -1
-  auto load_item = [&](int it, int& np, int& h, int& pidx, int& last) {
-    np = 0; h = 0; pidx = 0; last = -1;
+  auto load_item = [&](int it, int& np, int& h, int& pidx, int& pidx2, int& last) {
+    np = 0; h = 0; pidx = 0; pidx2 = 0; last = -1;
     if (it < n_items) {
       const Item L = decode_item(p, it);
       np = L.np; h = L.h;
       if (np > 0 && L.page0 + np == (L.seq_len + p.P - 1) / p.P) last = np - 1;
-      if (lane < L.np) pidx = p.page_table[(size_t)L.b * p.max_pages + L.page0 + lane];
+      const int32_t* row = p.page_table + (size_t)L.b * p.max_pages + L.page0;
+      if (lane < L.np) pidx = row[lane];
+      if (32 + lane < L.np) pidx2 = row[32 + lane];
     }
   };
-  load_item(cur, cur_np, cur_h, pidx_cur, cur_last);
-  load_item(nxt, nxt_np, nxt_h, pidx_nxt, nxt_last);
+  load_item(cur, cur_np, cur_h, pidx_cur, pidx_cur2, cur_last);
+  load_item(nxt, nxt_np, nxt_h, pidx_nxt, pidx_nxt2, nxt_last);
   // loader: `lq` = stream position of the next page to issue, counted from cur's first page
   // (pages past cur's end belong to nxt); stages are used in order, one mbarrier each.
   // Before griddepcontrol.wait (decode step) a sequence's last page is not loaded: the
@@ -255,7 +258,9 @@ attend_partial_mma(AttnParams p, int S) {
     const int kn = lq - cur_np;
     if (!in_cur && kn >= nxt_np) return false;
     if (!waited && p.protect_last && (in_cur ? lq == cur_last : kn == nxt_last)) return false;
-    const int64_t page = __shfl_sync(0xffffffffu, in_cur ? pidx_cur : pidx_nxt, in_cur ? lq : kn);
+    const int li = in_cur ? lq : kn;
+    const int64_t page = __shfl_sync(0xffffffffu, in_cur ? (li < 32 ? pidx_cur : pidx_cur2)
+                                                         : (li < 32 ? pidx_nxt : pidx_nxt2), li & 31);
     const int h = in_cur ? cur_h : nxt_h;
     if (lane == 0)
       bulk_load(ring + (size_t)s_issue * page_bytes, p.pool + (page * p.hkv + h) * (int64_t)page_bytes,
@@ -833,9 +838,9 @@ attend_partial_mma(AttnParams p, int S) {
     // ---- advance: the loader already moved on to `nxt`
     lq -= cur_np;
     cur = nxt;
-    cur_np = nxt_np; cur_h = nxt_h; pidx_cur = pidx_nxt; cur_last = nxt_last;
+    cur_np = nxt_np; cur_h = nxt_h; pidx_cur = pidx_nxt; pidx_cur2 = pidx_nxt2; cur_last = nxt_last;
     nxt = cur < n_items ? bcast(pending) : n_items;
-    load_item(nxt, nxt_np, nxt_h, pidx_nxt, nxt_last);
+    load_item(nxt, nxt_np, nxt_h, pidx_nxt, pidx_nxt2, nxt_last);
     pending = nxt < n_items ? fetch_async() : 0;
     while (inflight < S && issue_one()) {}
   }

@@ -134,10 +134,11 @@ __global__ void __launch_bounds__(512) attend_prologue_kernel(PrologueParams pp)
     float mx = fmaxf(fmaxf(fabsf(a.x), fabsf(a.y)), fmaxf(fabsf(a.z), fabsf(a.w)));
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     const float s = mx > 0.f ? mx / 32639.f : 1.f;
-    const int v0 = max(-32639, min(32639, __float2int_rn(a.x / s)));
-    const int v1 = max(-32639, min(32639, __float2int_rn(a.y / s)));
-    const int v2 = max(-32639, min(32639, __float2int_rn(a.z / s)));
-    const int v3 = max(-32639, min(32639, __float2int_rn(a.w / s)));
+    const float is = mx > 0.f ? 32639.f / mx : 1.f;   // one division; the clamp absorbs rounding
+    const int v0 = max(-32639, min(32639, __float2int_rn(a.x * is)));
+    const int v1 = max(-32639, min(32639, __float2int_rn(a.y * is)));
+    const int v2 = max(-32639, min(32639, __float2int_rn(a.z * is)));
+    const int v3 = max(-32639, min(32639, __float2int_rn(a.w * is)));
     const uint2 pk = make_uint2((uint32_t)(v0 & 0xffff) | ((uint32_t)v1 << 16),
                                 (uint32_t)(v2 & 0xffff) | ((uint32_t)v3 << 16));
     reinterpret_cast<uint2*>(pp.qint + row * kD)[lane] = pk;

@@ -370,12 +370,6 @@ __global__ void __launch_bounds__(256) attend_merge_kernel(AttnParams p, const f
                  : "memory");
   }
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
-#ifdef OSCAR_MERGE_EMPTY   // A/B builds only: launch + dependency cost of the merge
-  if (RV) {
-    asm volatile("{\n.reg .pred P1;\nWAIT_E%=:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n@!P1 bra WAIT_E%=;\n}\n" ::"r"(msmem_u32(&bar)) : "memory");
-  }
-  return;
-#endif
   const int ns = p.n_splits;
   {
     const int hd = w % GQ, part = w / GQ;
@@ -688,7 +682,6 @@ cudaError_t launch_attend(const oscar_ctx& c, const void* q, const int32_t* page
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
-#ifndef OSCAR_SKIP_MERGE   // (A/B builds only: measures the merge's share of attend)
   {
     void (*fn)(AttnParams, const float*, void*, int, float*) =
         c.g == 1 ? attend_merge_kernel<1> : c.g == 2 ? attend_merge_kernel<2>
@@ -706,7 +699,6 @@ cudaError_t launch_attend(const oscar_ctx& c, const void* q, const int32_t* page
     e = cudaLaunchKernelEx(&cfg, fn, p, RV, out, out_fp32, lse);
     if (e != cudaSuccess) return e;
   }
-#endif
   return cudaGetLastError();
 }
 

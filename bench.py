@@ -92,6 +92,21 @@ class ClockSampler:
                 "samples": len(s)}
 
 
+def ncu_kernel(name):
+    """(duration µs, DRAM bytes) of one kernel from the committed ncu capture, or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            j = json.load(f)
+        for k, v in j["kernels"].items():
+            if k.startswith(name):
+                d = v[0]
+                scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
+                return d["duration"] * scale.get(d.get("duration_unit", "us"), 1.0), d["traffic_bytes"]
+    except Exception:
+        pass
+    return None
+
+
 def ncu_traffic(kernels):
     """DRAM bytes per launch (read + write) of the named kernels, summed, from the committed
     `ncu --set full` capture (profiles/ncu_traffic.json, written by tools/ncu_traffic.py)."""
@@ -584,6 +599,13 @@ def main():
                      "algorithmic_bytes_per_launch": dec_bytes, "avg_launch_us": dec_ms * 1e3,
                      "avg_launch_us_source": "timed region / (steps x layers): the step is only decode_step calls",
                      "avg_launch_us_per_call_events": dec_ms_events * 1e3, "peak_kind": peak_kind},
+        "streaming_kernel_ncu": (lambda r: None if r is None else {
+            "kernel": "attend_partial_mma (85 % of the decode step)", "duration_us": r[0],
+            "algorithmic_bytes": B_ * L_ * HKV * TOKHEAD_BYTES, "dram_bytes": r[1],
+            "GBps": B_ * L_ * HKV * TOKHEAD_BYTES / r[0] / 1e3,
+            "frac": B_ * L_ * HKV * TOKHEAD_BYTES / r[0] / 1e3 / hbm_peak,
+            "source": "profiles/ncu_traffic.json: ncu --set full, serialised launch (not a bench timing)"})(
+            ncu_kernel("attend_partial_mma")),
         "attend_only": {"avg_launch_us": attn_ms * 1e3, "GBps": attn_gbs, "frac": attn_gbs / hbm_peak,
                         "algorithmic_bytes_per_launch": attn_bytes,
                         "kernel": "oscar_attend (prologue + partial + merge)"},

@@ -130,7 +130,8 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
   extern __shared__ uint8_t smem_raw[];
   TcSmem& S = *reinterpret_cast<TcSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // PDL: a following attend's q_rotate_kernel reads none of our outputs; let it start now
+  // PDL: a following kernel may launch now (the attend prologue is launched without PDL and so
+  // still starts after this kernel completes)
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   const int pair = blockIdx.x / p.cpp, sub = blockIdx.x % p.cpp;
   const int h = pair >> 1, isV = pair & 1;

@@ -10,7 +10,7 @@
 // finishes).  Per page, in chunks of up to 64 tokens:
 //   QK  : IMMA m16n8k32 s8 x u8 -> s32.  A = q̃ quantized to 15 bits and split hi/lo int8
 //         (rows = (hi|lo) x (group, head) "combos", zero outside the combo's group; built once
-//         per (b, h) by q_rotate_kernel), B = the raw 2/4-bit codes moved to the top bits of
+//         per (b, h) by attend_prologue_kernel), B = the raw 2/4-bit codes moved to the top bits of
 //         each byte (a left shift = IMAD on the FMA pipe, + one LOP3 per 4 codes; the 2^(8-b)
 //         byte scale is folded into qscale / qsum).  Exact integer dots per (token, head, group); the fp32
 //         epilogue applies s_K, m_K (x̂ = s·c + m).
@@ -224,7 +224,7 @@ attend_partial_mma(AttnParams p, int S) {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(policy));
 
   // work items: the first two per warp are static (no atomic latency at start), the rest are
-  // pulled from the counter (reset to 0 by q_rotate_kernel) offset by 2·(total warps)
+  // pulled from the counter (reset to 0 by attend_prologue_kernel) offset by 2·(total warps)
   const int n_items = p.n_items;
   const int total_warps = gridDim.x * kWarps, gw = blockIdx.x * kWarps + warp;
   auto fetch_async = [&]() { return lane == 0 ? atomicAdd(p.work, 1) + 2 * total_warps : 0; };
@@ -270,7 +270,7 @@ attend_partial_mma(AttnParams p, int S) {
     ++inflight;
     return true;
   };
-  // the first pages depend only on the caller's inputs: start streaming before q_rotate ends
+  // the first pages depend only on the caller's inputs: start streaming before the prologue ends
   while (inflight < S && issue_one()) {}
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   waited = true;
@@ -928,8 +928,8 @@ cudaError_t launch_attend_mma(const AttnParams& p, int total_warps, cudaStream_t
   if (e != cudaSuccess) return e;
   int warps = total_warps < p.n_items ? total_warps : p.n_items;
   const int grid = (warps + kWarps - 1) / kWarps;
-  // programmatic dependent launch: the first page loads overlap q_rotate_kernel's tail;
-  // griddepcontrol.wait in the kernel orders every read of q_rotate's outputs
+  // programmatic dependent launch: the first page loads overlap attend_prologue_kernel;
+  // griddepcontrol.wait in the kernel orders every read of the prologue's outputs
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kWarps * 32);

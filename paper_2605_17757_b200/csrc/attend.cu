@@ -332,8 +332,9 @@ __global__ void __launch_bounds__(128) attend_partial_simple(AttnParams p) {
 
 // ------------------------------------------------------------------ merge
 // LSE merge of the split-K partials + un-rotation o = õ·R_Vᵀ (reading Z21).
-// grid (B, H_kv), 256 threads (8 warps): one CTA per (sequence, KV head), so the g query heads
-// of the group share one copy of R_V[h].  Before griddepcontrol.wait (it only touches the
+// grid (B, H_kv, g / HC), 256 threads (8 warps): one CTA per (sequence, KV head) and HC query
+// heads of its group — HC = g normally (the heads share one copy of R_V[h]), HC = 1 for small
+// batches (more CTAs, more warps per head's splits).  Before griddepcontrol.wait (it only touches the
 // caller's inputs) R_V[h] (64 KB) is bulk-copied into smem.  Then warp w serves head w mod g,
 // splits s ≡ w / g (mod 8/g): each lane issues all loads of a batch of up to 16 splits at once
 // (partial row float4 = channels 4l..4l+3, split max and sum) and folds them with a running max;
@@ -346,19 +347,20 @@ __device__ __forceinline__ uint32_t msmem_u32(const void* ptr) {
 }
 }  // namespace
 
-template <int GQ>
+template <int HC>
 __global__ void __launch_bounds__(256) attend_merge_kernel(AttnParams p, const float* __restrict__ RV,
                                                            void* __restrict__ out, int out_fp32,
                                                            float* __restrict__ lse) {
-  constexpr int WPH = 8 / GQ;                        // warps per query head
+  constexpr int WPH = 8 / HC;                        // warps per query head
   constexpr int NB = 8;                              // splits per load batch (two in flight) per warp
-  constexpr int HPT = (GQ + 1) / 2;                  // heads per thread in the un-rotation
+  constexpr int HPT = (HC + 1) / 2;                  // heads per thread in the un-rotation
   extern __shared__ __align__(128) float Rs[];       // [128][128] R_V[h]
   __shared__ __align__(16) float po[8][kD];
-  __shared__ __align__(16) float ot[GQ][kD];
-  __shared__ float pm[8], pl[8], sws[GQ];
+  __shared__ __align__(16) float ot[HC][kD];
+  __shared__ float pm[8], pl[8], sws[HC];
   __shared__ __align__(8) uint64_t bar;
   const int b = blockIdx.x, h = blockIdx.y, tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const int hz = blockIdx.z * HC;                    // first query head (within the group) of this CTA
   if (RV && tid == 0) {
     const uint32_t bb = msmem_u32(&bar);
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bb));
@@ -372,8 +374,8 @@ __global__ void __launch_bounds__(256) attend_merge_kernel(AttnParams p, const f
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   const int ns = p.n_splits;
   {
-    const int hd = w % GQ, part = w / GQ;
-    const size_t rbh = (size_t)b * p.hq + (size_t)h * GQ + hd;
+    const int hd = w % HC, part = w / HC;
+    const size_t rbh = (size_t)b * p.hq + (size_t)h * p.g + hz + hd;
     auto prow = [&](int s) -> size_t { return rbh * ns + s; };
     float mw = -INFINITY, Lw = 0.f;
     float4 ow = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -423,19 +425,19 @@ __global__ void __launch_bounds__(256) attend_merge_kernel(AttnParams p, const f
   }
   __syncthreads();
   const bool seg = p.seg_o != nullptr;
-  for (int e = tid; e < GQ * kD; e += 256) {
+  for (int e = tid; e < HC * kD; e += 256) {
     const int hd = e >> 7, c = e & (kD - 1);
-    const size_t row = (size_t)b * p.hq + (size_t)h * GQ + hd;
+    const size_t row = (size_t)b * p.hq + (size_t)h * p.g + hz + hd;
     float M = seg ? p.seg_m[row] : -INFINITY;
 #pragma unroll
-    for (int j = 0; j < WPH; ++j) M = fmaxf(M, pm[hd + GQ * j]);
+    for (int j = 0; j < WPH; ++j) M = fmaxf(M, pm[hd + HC * j]);
     float L = 0.f, o = 0.f;
     if (M != -INFINITY) {
 #pragma unroll
       for (int j = 0; j < WPH; ++j) {
-        const float wj = exp2f(pm[hd + GQ * j] - M);
-        L = fmaf(pl[hd + GQ * j], wj, L);
-        o = fmaf(po[hd + GQ * j][c], wj, o);
+        const float wj = exp2f(pm[hd + HC * j] - M);
+        L = fmaf(pl[hd + HC * j], wj, L);
+        o = fmaf(po[hd + HC * j][c], wj, o);
       }
     }
     const float wseg = (seg && M != -INFINITY) ? exp2f(p.seg_m[row] - M) : 0.f;
@@ -466,7 +468,7 @@ __global__ void __launch_bounds__(256) attend_merge_kernel(AttnParams p, const f
 #pragma unroll
       for (int j = 0; j < HPT; ++j) {
         const int hd = hh + 2 * j;
-        if (hd < GQ) {
+        if (hd < HC) {
           const float4 x = reinterpret_cast<const float4*>(ot[hd])[c4];
           acc[j] = fmaf(r.x, x.x, fmaf(r.y, x.y, fmaf(r.z, x.z, fmaf(r.w, x.w, acc[j]))));
         }
@@ -474,13 +476,13 @@ __global__ void __launch_bounds__(256) attend_merge_kernel(AttnParams p, const f
     }
   } else {                                           // pre-rotated V (NEXT-2): o = õ
 #pragma unroll
-    for (int j = 0; j < HPT; ++j) acc[j] = hh + 2 * j < GQ ? ot[hh + 2 * j][cp] : 0.f;
+    for (int j = 0; j < HPT; ++j) acc[j] = hh + 2 * j < HC ? ot[hh + 2 * j][cp] : 0.f;
   }
 #pragma unroll
   for (int j = 0; j < HPT; ++j) {
     const int hd = hh + 2 * j;
-    if (hd >= GQ) continue;
-    const size_t row = (size_t)b * p.hq + (size_t)h * GQ + hd;
+    if (hd >= HC) continue;
+    const size_t row = (size_t)b * p.hq + (size_t)h * p.g + hz + hd;
     float v = acc[j];
     if (seg) v = fmaf(p.seg_o[row * kD + cp], sws[hd], v);
     const size_t idx = row * kD + cp;
@@ -683,14 +685,18 @@ cudaError_t launch_attend(const oscar_ctx& c, const void* q, const int32_t* page
     if (e != cudaSuccess) return e;
   }
   {
+    // small batches: one CTA per query head (the fold of many splits gets 8 warps per head)
+    const bool per_head = (long)B * c.hkv * 4 <= (long)c.num_sms;
     void (*fn)(AttnParams, const float*, void*, int, float*) =
-        c.g == 1 ? attend_merge_kernel<1> : c.g == 2 ? attend_merge_kernel<2>
+        per_head ? attend_merge_kernel<1>
+      : c.g == 1 ? attend_merge_kernel<1> : c.g == 2 ? attend_merge_kernel<2>
       : c.g == 4 ? attend_merge_kernel<4> : attend_merge_kernel<8>;
+    const int hc = per_head ? 1 : c.g;
     const int msmem = RV ? kD * kD * 4 : 0;
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, msmem);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3((unsigned)B, (unsigned)c.hkv);
+    cfg.gridDim = dim3((unsigned)B, (unsigned)c.hkv, (unsigned)(c.g / hc));
     cfg.blockDim = dim3(256);
     cfg.dynamicSmemBytes = msmem;
     cfg.stream = s;

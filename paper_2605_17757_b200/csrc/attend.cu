@@ -70,6 +70,17 @@ __global__ void __launch_bounds__(512) attend_prologue_kernel(PrologueParams pp)
   const int w = tid >> 5, lane = tid & 31;
   const int G = 1 << pp.lgG;
   const bool dec = pp.knew != nullptr;
+  // decode step: the new row's slot (two dependent global loads) is fetched first, so its
+  // latency hides behind the R loads instead of sitting on the append's critical path
+  int slot_L = 0;
+  int64_t slot_new = 0;
+  if (dec && w >= 14) {
+    slot_L = pp.seq_lens[b];
+    if (slot_L > 0) {
+      const int pos = slot_L - 1;
+      slot_new = (int64_t)pp.page_table[(size_t)b * pp.max_pages + pos / pp.ep.P] * pp.ep.P + pos % pp.ep.P;
+    }
+  }
   if (pp.work && b == 0 && h == 0 && tid == 0) *pp.work = 0;   // reset the work-item counter
   // this warp's 8 rows of R_K (and R_V) are loaded first: their latency overlaps the row loads
   const bool rv = dec && pp.RV;
@@ -149,13 +160,10 @@ __global__ void __launch_bounds__(512) attend_prologue_kernel(PrologueParams pp)
     if ((lane & ((G >> 2) - 1)) == 0) pp.qsum[row * 8 + (lane * 4 >> pp.lgG)] = gs;
   } else if (dec && w >= 14) {
     const int isV = w - 14;
-    const int L = pp.seq_lens[b];
-    if (L > 0) {
-      const int pos = L - 1;
-      const int64_t slot = (int64_t)pp.page_table[(size_t)b * pp.max_pages + pos / pp.ep.P] * pp.ep.P + pos % pp.ep.P;
+    if (slot_L > 0) {
       const float4 y4 = reinterpret_cast<const float4*>(ys[GQ + isV])[lane];
       float y[4] = {y4.x, y4.y, y4.z, y4.w};
-      quantize_store_row_warp(pp.ep, y, lane, slot, h, isV, pp.pool);
+      quantize_store_row_warp(pp.ep, y, lane, slot_new, h, isV, pp.pool);
     }
   }
   __syncthreads();

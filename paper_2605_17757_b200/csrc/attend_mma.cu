@@ -22,6 +22,7 @@
 //         masked straight into the fp16 mantissa (subnormal c·2^(b·q)·2^-24, exact), one LOP3
 //         per 2 codes, and each accumulator row is rescaled by 2^(24-b·q) at the end;
 //         B = p·s_V per (token, combo) column; the m_V term is a rank-1 FFMA sum.
+#include <mutex>
 #include <type_traits>
 
 #include "attend_common.cuh"
@@ -904,7 +905,10 @@ int attend_mma_total_warps(const oscar_ctx& c) {
   const int S = stages_for(c.page_bytes);
   const int smem = kWarps * S * (c.page_bytes + 8);
   // resident CTAs per SM, cached per (kernel, smem): the query is a few µs of host time
+  // (contexts may be used from several host threads: the cache is guarded)
+  static std::mutex mu;
   static struct { KernelFn fn; int smem, per_sm; } cache[16];
+  std::lock_guard<std::mutex> lock(mu);
   for (auto& e : cache)
     if (e.fn == fn && e.smem == smem) return c.num_sms * e.per_sm * kWarps;
   int per_sm = 0;

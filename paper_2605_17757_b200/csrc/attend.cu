@@ -504,7 +504,6 @@ __global__ void __launch_bounds__(256) attend_merge_kernel(AttnParams p, const f
 // sink + recent segment (§4, "an additional kernel for BF16 KV cache
 // attention"): scores q·k·scale·log2e in fp32 (lane = token), max / sum by warp shuffles,
 // p staged in smem, then Σ p v with lane = 4 channels.  Output in the ORIGINAL frame.
-constexpr int kSegCapMax = 1024;
 
 __global__ void __launch_bounds__(256) attend_segment_kernel(AttnParams p, const uint16_t* __restrict__ q,
                                                              const uint16_t* __restrict__ sk,

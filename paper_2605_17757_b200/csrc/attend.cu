@@ -6,6 +6,7 @@
 //                          (split, kv head, sequence)); the tensor-core kernel is in
 //                          attend_mma.cu (variant 0)
 //   attend_merge_kernel    LSE merge over splits, o = õ · R_Vᵀ, bf16/fp32 store, lse
+#include <type_traits>
 #include "common.cuh"
 #include "attend_common.cuh"
 #include "append_epilogue.cuh"
@@ -227,17 +228,23 @@ __global__ void __launch_bounds__(512) attend_prologue_kernel(PrologueParams pp)
 // grid (n_splits, H_kv, B); 128 threads (thread c <-> channel c in PV).  Page-by-page:
 // stage the (page, head) block in smem, scores for all (token, head) pairs, online softmax
 // per head (log2 domain), PV accumulation in registers.
+// The K row is read as 32-bit words: channels 32j..32j+31 are the BITS words BITS·j.. of the
+// row (little-endian bit stream, codes straddling words taken with a funnel shift); one
+// 32-channel chunk never crosses a quantization group (G ∈ {32, 64, 128}).  PV reads the V
+// codes of a 4-token group with one 32-bit load per byte column (fmt_vbyte interleaving).
+template <int BITS, int GQ>
 __global__ void __launch_bounds__(128) attend_partial_simple(AttnParams p) {
   extern __shared__ __align__(16) unsigned char sm_raw[];
   float* qs = reinterpret_cast<float*>(sm_raw);              // [g][128]
   float* qsum = qs + 8 * kD;                                  // [g][ng]
-  float* sc = qsum + 8 * 8;                                   // [g][P]
+  float* sc = qsum + 8 * 8;                                   // [P][g]
   float* mrun = sc + 8 * p.P;                                 // [g]
   float* lrun = mrun + 8;                                     // [g]
   float* alpha = lrun + 8;                                    // [g]
   uint8_t* pg = reinterpret_cast<uint8_t*>(alpha + 8);        // page block
   const int split = blockIdx.x, h = blockIdx.y, b = blockIdx.z, tid = threadIdx.x;
-  const int g = p.g, P = p.P;
+  constexpr int g = GQ;
+  const int P = p.P;
   const int seq_len = p.seq_lens[b];
   const int page0 = split * p.pps;
   const int page1 = min(page0 + p.pps, (seq_len + P - 1) / P);
@@ -252,9 +259,12 @@ __global__ void __launch_bounds__(128) attend_partial_simple(AttnParams p) {
     for (int c = grp * p.G; c < (grp + 1) * p.G; ++c) s += qs[i * kD + c];
     qsum[i * 8 + grp] = s;
   }
-  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  float acc[GQ];
+#pragma unroll
+  for (int i = 0; i < GQ; ++i) acc[i] = 0.f;
   const int qmax = (1 << p.bits) - 1;
   const int rb = p.row_bytes;
+  const int ns = 128 % P == 0 ? min(128 / P, g) : 0;
 
   for (int pi = page0; pi < page1; ++pi) {
     __syncthreads();
@@ -264,27 +274,62 @@ __global__ void __launch_bounds__(128) attend_partial_simple(AttnParams p) {
     __syncthreads();
     const int valid = min(P, seq_len - pi * P);
     const uint8_t* meta = pg + p.meta_off;
-    // scores
-    for (int e = tid; e < g * P; e += 128) {
-      const int i = e / P, t = e % P;
-      float s = -INFINITY;
-      if (t < valid) {
-        s = 0.f;
-        const uint8_t* krow = pg + fmt_krow(t) * rb;
-        for (int grp = 0; grp < p.ng; ++grp) {
-          float dot = 0.f;
-          for (int c = grp * p.G; c < (grp + 1) * p.G; ++c) {
-            const int bit = c * p.bits, jb = bit >> 3, sh = bit & 7;
-            int word = krow[jb];
-            if (sh + p.bits > 8) word |= krow[jb + 1] << 8;   // 3-bit codes straddle bytes
-            const int code = (word >> sh) & qmax;
-            dot = fmaf(qs[i * kD + c], (float)code, dot);
+    // scores: thread -> token t and heads i0, i0 + ns, ... (the code unpack is shared by
+    // the heads); ns = 128 / P thread slices when P divides 128, else one (t, head) pair each
+    auto score_token = [&](auto NHc, int t, int i0, int istep) {
+      constexpr int nh = decltype(NHc)::value;
+      if (t >= valid) {
+#pragma unroll
+        for (int k = 0; k < nh; ++k) sc[t * GQ + i0 + k * istep] = -INFINITY;
+        return;
+      }
+      const uint32_t* kw = reinterpret_cast<const uint32_t*>(pg + fmt_krow(t) * rb);
+      float s[nh], dot[nh];
+#pragma unroll
+      for (int k = 0; k < nh; ++k) { s[k] = 0.f; dot[k] = 0.f; }
+#pragma unroll 1
+      for (int j = 0; j < kD / 32; ++j) {
+        uint32_t w[BITS + 1];
+#pragma unroll
+        for (int u = 0; u < BITS; ++u) w[u] = kw[BITS * j + u];
+        w[BITS] = 0u;
+#pragma unroll
+        for (int k4 = 0; k4 < 8; ++k4) {
+          float4 qv[nh];
+#pragma unroll
+          for (int k = 0; k < nh; ++k)
+            qv[k] = reinterpret_cast<const float4*>(qs + (i0 + k * istep) * kD)[8 * j + k4];
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            const int bit = BITS * (4 * k4 + r), wi = bit >> 5, sh = bit & 31;
+            const uint32_t v = sh + BITS <= 32 ? (w[wi] >> sh) : __funnelshift_r(w[wi], w[wi + 1], sh);
+            const float cf = (float)(v & ((1u << BITS) - 1u));
+#pragma unroll
+            for (int k = 0; k < nh; ++k)
+              dot[k] = fmaf(r == 0 ? qv[k].x : r == 1 ? qv[k].y : r == 2 ? qv[k].z : qv[k].w, cf, dot[k]);
           }
+        }
+        if ((32 * (j + 1)) % p.G == 0) {
+          const int grp = (32 * j) / p.G;
           const __half* mt = reinterpret_cast<const __half*>(meta + fmt_meta(t, grp, p.ng));
-          s += __half2float(mt[0]) * dot + __half2float(mt[1]) * qsum[i * 8 + grp];
+          const float sK = __half2float(mt[0]), mK = __half2float(mt[1]);
+#pragma unroll
+          for (int k = 0; k < nh; ++k) {
+            s[k] += sK * dot[k] + mK * qsum[(i0 + k * istep) * 8 + grp]; dot[k] = 0.f; }
         }
       }
-      sc[i * P + t] = s;
+#pragma unroll
+      for (int k = 0; k < nh; ++k) sc[t * GQ + i0 + k * istep] = s[k];
+    };
+    using I1 = std::integral_constant<int, 1>;
+    if (ns > 0 && tid / P < ns) {
+      const int nh = g / ns;
+      if constexpr (g >= 8) { if (nh == 8) score_token(std::integral_constant<int, 8>{}, tid % P, tid / P, ns); }
+      if constexpr (g >= 4) { if (nh == 4) score_token(std::integral_constant<int, 4>{}, tid % P, tid / P, ns); }
+      if constexpr (g >= 2) { if (nh == 2) score_token(std::integral_constant<int, 2>{}, tid % P, tid / P, ns); }
+      if (nh == 1) score_token(I1{}, tid % P, tid / P, ns);
+    } else if (ns == 0) {
+      for (int e = tid; e < g * P; e += 128) score_token(I1{}, e % P, e / P, 1);
     }
     __syncthreads();
     // online softmax per head: warp w handles heads w, w+4
@@ -292,13 +337,13 @@ __global__ void __launch_bounds__(128) attend_partial_simple(AttnParams p) {
       const int warp = tid >> 5, lane = tid & 31;
       for (int i = warp; i < g; i += 4) {
         float mx = -INFINITY;
-        for (int t = lane; t < P; t += 32) mx = fmaxf(mx, sc[i * P + t]);
+        for (int t = lane; t < P; t += 32) mx = fmaxf(mx, sc[t * GQ + i]);
         for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
         const float mnew = fmaxf(mrun[i], mx);
         float sum = 0.f;
         for (int t = lane; t < P; t += 32) {
-          const float pv = exp2f(sc[i * P + t] - mnew);
-          sc[i * P + t] = pv;
+          const float pv = exp2f(sc[t * GQ + i] - mnew);
+          sc[t * GQ + i] = pv;
           sum += pv;
         }
         for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
@@ -318,19 +363,29 @@ __global__ void __launch_bounds__(128) attend_partial_simple(AttnParams p) {
       const int grp = c / p.G;
       const int bit = c * p.bits;
       const int jb = bit >> 3, sh = bit & 7;
+#pragma unroll
       for (int i = 0; i < g; ++i) acc[i] *= alpha[i];
-      for (int t = 0; t < valid; ++t) {
-        int word = pg[p.vcodes_off + fmt_vbyte(t, jb, rb)];
-        if (sh + p.bits > 8) word |= pg[p.vcodes_off + fmt_vbyte(t, jb + 1, rb)] << 8;
-        const int code = (word >> sh) & qmax;
-        const __half* mt = reinterpret_cast<const __half*>(meta + fmt_meta(t, grp, p.ng) + 16);
-        const float v = fmaf(__half2float(mt[0]), (float)code, __half2float(mt[1]));
-        for (int i = 0; i < g; ++i) acc[i] = fmaf(sc[i * P + t], v, acc[i]);
+      for (int t4 = 0; t4 < valid; t4 += 4) {
+        const uint32_t w0 = *reinterpret_cast<const uint32_t*>(pg + p.vcodes_off + fmt_vbyte(t4, jb, rb));
+        const uint32_t w1 = sh + BITS > 8
+            ? *reinterpret_cast<const uint32_t*>(pg + p.vcodes_off + fmt_vbyte(t4, jb + 1, rb)) : 0u;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int t = t4 + u;
+          if (t >= valid) break;
+          const uint32_t word = ((w0 >> (8 * u)) & 0xffu) | (((w1 >> (8 * u)) & 0xffu) << 8);
+          const int code = (int)((word >> sh) & (uint32_t)qmax);
+          const __half* mt = reinterpret_cast<const __half*>(meta + fmt_meta(t, grp, p.ng) + 16);
+          const float v = fmaf(__half2float(mt[0]), (float)code, __half2float(mt[1]));
+#pragma unroll
+          for (int i = 0; i < g; ++i) acc[i] = fmaf(sc[t * GQ + i], v, acc[i]);
+        }
       }
     }
   }
   __syncthreads();
   // partial outputs
+#pragma unroll
   for (int i = 0; i < g; ++i) {
     const size_t row = ((size_t)b * p.hq + h * g + i) * p.n_splits + split;
     p.ws_o[row * kD + tid] = acc[i];
@@ -672,9 +727,13 @@ cudaError_t launch_attend(const oscar_ctx& c, const void* q, const int32_t* page
   p.protect_last = k_new != nullptr;
   if (!mma) {
     const int smem = (8 * kD + 64 + 8 * c.P + 24) * 4 + c.page_bytes;
-    e = cudaFuncSetAttribute(attend_partial_simple, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+#define OSCAR_SIMPLE(BB) (c.g == 1 ? attend_partial_simple<BB, 1> : c.g == 2 ? attend_partial_simple<BB, 2> \
+                               : c.g == 4 ? attend_partial_simple<BB, 4> : attend_partial_simple<BB, 8>)
+    void (*sfn)(AttnParams) = c.bits == 2 ? OSCAR_SIMPLE(2) : c.bits == 3 ? OSCAR_SIMPLE(3) : OSCAR_SIMPLE(4);
+#undef OSCAR_SIMPLE
+    e = cudaFuncSetAttribute(sfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    attend_partial_simple<<<dim3(p.n_splits, c.hkv, B), 128, smem, s>>>(p);
+    sfn<<<dim3(p.n_splits, c.hkv, B), 128, smem, s>>>(p);
   } else {
     e = launch_attend_mma(p, attend_mma_total_warps(c), s);
     if (e != cudaSuccess) return e;

@@ -1,6 +1,7 @@
 """Time oscar_attend / oscar_decode_step variants on the C2 decode workload (GPU box):
 python tools/attend_probe.py  ->  per-call µs for attend with R_V, attend with R_V = NULL
-(no un-rotation: isolates the merge's R_V work) and decode_step."""
+(no un-rotation: isolates the merge's R_V work) and decode_step.  OSCAR_PROBE_BITS picks the
+code width (default 2)."""
 import os
 import sys
 
@@ -10,11 +11,12 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2605_17757_b200 import binding as Bnd, synth  # noqa: E402
 
 B, L, HQ, HKV, D, P, NL = 16, 32768, 32, 8, 128, 64, 8
+BITS = int(os.environ.get("OSCAR_PROBE_BITS", "2"))
 dev = "cuda"
-o = Bnd.Oscar(Bnd.Config(num_q_heads=HQ, num_kv_heads=HKV, bits=2, group_size=64, page_size=P))
+o = Bnd.Oscar(Bnd.Config(num_q_heads=HQ, num_kv_heads=HKV, bits=BITS, group_size=64, page_size=P))
 gen = torch.Generator(device=dev).manual_seed(3)
 mp = L // P
-pools = [synth.torch_random_pool(gen, B * mp, HKV, o.page_bytes(), 2 * P * 32, P * 2, dev) for _ in range(NL)]
+pools = [synth.torch_random_pool(gen, B * mp, HKV, o.page_bytes(), 2 * P * 16 * BITS, P * 2, dev) for _ in range(NL)]
 pt = torch.arange(B * mp, dtype=torch.int32, device=dev).reshape(B, mp)
 sl = torch.full((B,), L, dtype=torch.int32, device=dev)
 RK = [synth.torch_rotation(gen, HKV, D, dev) for _ in range(NL)]
@@ -48,7 +50,7 @@ print("decode_step %.2f us" % timeit(lambda l: o.decode_step(q[l], k[l], v[l], p
 
 if len(sys.argv) > 1:      # pages-per-split sweep: python tools/attend_probe.py 8 16 32
     for pps in map(int, sys.argv[1:]):
-        o2 = Bnd.Oscar(Bnd.Config(num_q_heads=HQ, num_kv_heads=HKV, bits=2, group_size=64, page_size=P,
+        o2 = Bnd.Oscar(Bnd.Config(num_q_heads=HQ, num_kv_heads=HKV, bits=BITS, group_size=64, page_size=P,
                                   attend_pages_per_split=pps))
         ws2 = torch.empty(o2.attend_workspace_bytes(B, mp), dtype=torch.uint8, device=dev)
         print("pps %2d attend %.2f us" % (pps, timeit(lambda l: o2.attend(q[l], pt, sl, pools[l], RK[l], RV[l], ws2, out))))

@@ -242,6 +242,7 @@ __global__ void __launch_bounds__(128) attend_partial_simple(AttnParams p) {
   float* lrun = mrun + 8;                                     // [g]
   float* alpha = lrun + 8;                                    // [g]
   uint8_t* pg = reinterpret_cast<uint8_t*>(alpha + 8);        // page block
+  float2* vmf = reinterpret_cast<float2*>(pg + ((p.page_bytes + 15) & ~15));   // [P][ng]
   const int split = blockIdx.x, h = blockIdx.y, b = blockIdx.z, tid = threadIdx.x;
   constexpr int g = GQ;
   const int P = p.P;
@@ -274,6 +275,12 @@ __global__ void __launch_bounds__(128) attend_partial_simple(AttnParams p) {
     __syncthreads();
     const int valid = min(P, seq_len - pi * P);
     const uint8_t* meta = pg + p.meta_off;
+    // (s_V, m_V) of every (token, group) as float2, read by the PV loop (one LDS.64 per token)
+    for (int e = tid; e < valid * p.ng; e += 128) {
+      const int t = e / p.ng, grp = e - t * p.ng;
+      const __half2 h2 = *reinterpret_cast<const __half2*>(meta + fmt_meta(t, grp, p.ng) + 16);
+      vmf[e] = __half22float2(h2);
+    }
     // scores: thread -> token t and heads i0, i0 + ns, ... (the code unpack is shared by
     // the heads); ns = 128 / P thread slices when P divides 128, else one (t, head) pair each
     auto score_token = [&](auto NHc, int t, int i0, int istep) {
@@ -373,10 +380,10 @@ __global__ void __launch_bounds__(128) attend_partial_simple(AttnParams p) {
         for (int u = 0; u < 4; ++u) {
           const int t = t4 + u;
           if (t >= valid) break;
-          const uint32_t word = ((w0 >> (8 * u)) & 0xffu) | (((w1 >> (8 * u)) & 0xffu) << 8);
+          const uint32_t word = __byte_perm(w0, w1, u | ((4 + u) << 4));   // byte u of w0, w1
           const int code = (int)((word >> sh) & (uint32_t)qmax);
-          const __half* mt = reinterpret_cast<const __half*>(meta + fmt_meta(t, grp, p.ng) + 16);
-          const float v = fmaf(__half2float(mt[0]), (float)code, __half2float(mt[1]));
+          const float2 sm = vmf[t * p.ng + grp];
+          const float v = fmaf(sm.x, (float)code, sm.y);
 #pragma unroll
           for (int i = 0; i < g; ++i) acc[i] = fmaf(sc[t * GQ + i], v, acc[i]);
         }
@@ -726,7 +733,7 @@ cudaError_t launch_attend(const oscar_ctx& c, const void* q, const int32_t* page
   }
   p.protect_last = k_new != nullptr;
   if (!mma) {
-    const int smem = (8 * kD + 64 + 8 * c.P + 24) * 4 + c.page_bytes;
+    const int smem = (8 * kD + 64 + 8 * c.P + 24) * 4 + ((c.page_bytes + 15) & ~15) + c.P * (kD / c.G) * 8;
 #define OSCAR_SIMPLE(BB) (c.g == 1 ? attend_partial_simple<BB, 1> : c.g == 2 ? attend_partial_simple<BB, 2> \
                                : c.g == 4 ? attend_partial_simple<BB, 4> : attend_partial_simple<BB, 8>)
     void (*sfn)(AttnParams) = c.bits == 2 ? OSCAR_SIMPLE(2) : c.bits == 3 ? OSCAR_SIMPLE(3) : OSCAR_SIMPLE(4);

@@ -651,11 +651,16 @@ static int choose_pps(const oscar_ctx& c, int B, int max_pages) {
     pps = pps < lo ? lo : (pps > 64 ? 32 : pps);
     return (int)pps;
   }
-  const long target = (long)c.num_sms * 8;
+  // CUDA-core kernel: ~8 resident CTAs per SM; aim at ~8 waves of short splits (at least 4
+  // pages) so the last wave is a small fraction of the kernel (3-bit C2 shape: 52 -> 7 pages
+  // per split, 1.00 -> 0.81 ms)
+  const long target = (long)c.num_sms * 64;
   long splits = (target + units - 1) / units;
   if (splits < 1) splits = 1;
   if (splits > max_pages) splits = max_pages;
-  return (int)((max_pages + splits - 1) / splits);
+  long pps = (max_pages + splits - 1) / splits;
+  const long lo = max_pages < 4 ? (max_pages > 0 ? max_pages : 1) : 4;
+  return (int)(pps < lo ? lo : pps);
 }
 
 size_t attend_workspace_bytes(const oscar_ctx& c, int B, int max_pages) {

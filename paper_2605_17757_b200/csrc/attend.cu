@@ -376,16 +376,20 @@ __global__ void __launch_bounds__(128) attend_partial_simple(AttnParams p) {
         const uint32_t w0 = *reinterpret_cast<const uint32_t*>(pg + p.vcodes_off + fmt_vbyte(t4, jb, rb));
         const uint32_t w1 = sh + BITS > 8
             ? *reinterpret_cast<const uint32_t*>(pg + p.vcodes_off + fmt_vbyte(t4, jb + 1, rb)) : 0u;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        auto pv_tok = [&](int u) {
           const int t = t4 + u;
-          if (t >= valid) break;
           const uint32_t word = __byte_perm(w0, w1, u | ((4 + u) << 4));   // byte u of w0, w1
           const int code = (int)((word >> sh) & (uint32_t)qmax);
           const float2 sm = vmf[t * p.ng + grp];
           const float v = fmaf(sm.x, (float)code, sm.y);
 #pragma unroll
           for (int i = 0; i < g; ++i) acc[i] = fmaf(sc[t * GQ + i], v, acc[i]);
+        };
+        if (t4 + 4 <= valid) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) pv_tok(u);
+        } else {
+          for (int u = 0; u < valid - t4; ++u) pv_tok(u);
         }
       }
     }

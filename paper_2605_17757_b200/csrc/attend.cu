@@ -294,7 +294,7 @@ __global__ void __launch_bounds__(128) attend_partial_simple(AttnParams p) {
       float s[nh], dot[nh];
 #pragma unroll
       for (int k = 0; k < nh; ++k) { s[k] = 0.f; dot[k] = 0.f; }
-#pragma unroll 1
+#pragma unroll
       for (int j = 0; j < kD / 32; ++j) {
         uint32_t w[BITS + 1];
 #pragma unroll

@@ -91,7 +91,8 @@ OSCAR_API size_t oscar_page_bytes(const oscar_ctx* ctx);
  * Accumulate the unnormalized covariance targets of §3 for this call's N tokens:
  *   acc[h][0] += Σ_n Σ_{i in G_h} q_{n,i}ᵀ q_{n,i}        (C_Q)
  *   acc[h][1] += Σ_n Σ_{i in G_h} sv_{n,i}ᵀ sv_{n,i}      (C_S = VᵀSᵀSV = (SV)ᵀ(SV))
- * Q, SV: bf16 [N][H_q][d] row-major; SV is the per-query-head attention output S·V before
+ * Q, SV: bf16 [N][H_q][d] row-major (16-B aligned bases take the tcgen05 kernel, others the
+ * CUDA-core one); SV is the per-query-head attention output S·V before
  * W_O (C_S depends on S and V only through SV).  Query head i belongs to KV head i / g.
  * acc: fp64 [H_kv][2][d][d], caller-zeroed before the first call; each call ADDS.
  * Multi-GPU: shard tokens, then all-reduce acc (SUM) across ranks before finalize.
@@ -141,7 +142,8 @@ OSCAR_API oscar_status oscar_calib_clip(const oscar_ctx* ctx, const void* K, con
  * codes with fp16 (s, m) metadata (reading Z4 operation order), bit-pack, and store into
  * the slot's page block (FORMAT above).
  * K, V: bf16 [T][H_kv][d]; slots: int64 [T] (page·P + offset); R_K, R_V: fp32 [H_kv][d][d];
- * pool: see oscar_page_bytes.  T = 0 is a no-op.
+ * pool: see oscar_page_bytes.  T = 0 is a no-op.  K and V row bases 16-B aligned take the
+ * tensor-core kernel (TMA); other alignments are accepted and run the simple kernel.
  * R_V = NULL selects the pre-rotated-V mode ("absorb R_V into W_V"):
  * V rows are taken as already rotated (identity rotation); pass NULL to oscar_attend too. */
 OSCAR_API oscar_status oscar_quantize_append(const oscar_ctx* ctx, const void* K, const void* V,
@@ -155,7 +157,8 @@ OSCAR_API oscar_status oscar_quantize_append(const oscar_ctx* ctx, const void* K
  * o = õ·R_V[h]ᵀ.  Split-K over pages with an online-softmax merge.
  * q: bf16 [B][H_q][d]; page_table: int32 [B][max_pages]; seq_lens: int32 [B] (<= max_pages·P,
  * 0 => o = 0, lse = -inf); pool as written by oscar_quantize_append; workspace: device bytes
- * >= oscar_attend_workspace_bytes(ctx, B, max_pages); out: [B][H_q][d] bf16 (out_fp32 = 0)
+ * >= oscar_attend_workspace_bytes(ctx, B, max_pages), 256-B aligned (its sub-buffers are laid
+ * out on 256-B boundaries; a base not 16-B aligned -> OSCAR_ERR_ARG); out: [B][H_q][d] bf16 (out_fp32 = 0)
  * or fp32 (out_fp32 = 1); lse: fp32 [B][H_q] natural-log sum-exp of ℓ, or NULL.
  * R_V = NULL (pre-rotated-V mode, NEXT-2): o = õ, returned in V's own (rotated) frame. */
 OSCAR_API size_t oscar_attend_workspace_bytes(const oscar_ctx* ctx, int32_t B, int32_t max_pages);
@@ -196,11 +199,17 @@ OSCAR_API oscar_status oscar_attend_mixed(const oscar_ctx* ctx, const void* q, c
                                 void* stream);
 
 /* ---------------------------------------------------------------- test hooks
- * Stage-isolated entry points used by the parity tests (same kernels, other I/O).
- * oscar_rotate: Xrot[t][h][:] = X[t][h][:] · R[h] in fp32 (App A.5).
- *   X: bf16 [T][H_kv][d]; R: fp32 [H_kv][d][d]; Xrot: fp32 [T][H_kv][d].
- * oscar_quantize_rotated: clip + quantize + pack + store of already-rotated fp32 rows
- *   (skips the rotation: "identical rotated inputs"); Krot, Vrot: fp32 [T][H_kv][d]. */
+ * Stage-isolated entry points used by the parity tests.  Each takes the kernel route that
+ * oscar_quantize_append takes for the same T and context (variant 0: T <= 64 -> the decode-size
+ * kernel, else the tcgen05 kernel when no clipping is configured; variant 1, clipping, or row
+ * bases that are not 16-B aligned -> the simple CUDA-core kernel), so the stages checked are
+ * those of the kernel that writes the pool.
+ * oscar_rotate: Xrot[t][h][:] = X[t][h][:] · R[h] in fp32 (App A.5), exactly the
+ *   rotated values that kernel's epilogue would quantize (tcgen05: the fp32 TMEM accumulator of
+ *   [x x]·[R_hi; R_lo]).  X: bf16 [T][H_kv][d]; R: fp32 [H_kv][d][d]; Xrot: fp32 [T][H_kv][d].
+ * oscar_quantize_rotated: clip + quantize + pack + store of already-rotated fp32 rows through
+ *   that kernel's own epilogue (skips the rotation: "identical rotated inputs"); Krot, Vrot:
+ *   fp32 [T][H_kv][d]. */
 OSCAR_API oscar_status oscar_rotate(const oscar_ctx* ctx, const void* X, const float* R, float* Xrot,
                           int64_t T, void* stream);
 OSCAR_API oscar_status oscar_quantize_rotated(const oscar_ctx* ctx, const float* Krot, const float* Vrot,

@@ -17,8 +17,8 @@ import numpy as np
 __all__ = [
     "hadamard", "bit_reversal", "eigh_desc", "compose_rotation", "pbr_placement",
     "cov_accumulate", "score_value", "calibrate_from_sums", "rotate", "clip_index",
-    "clip_rows", "quantize_rows", "dequantize_rows", "pack_codes", "unpack_codes",
-    "PageFormat", "quantize_rotated", "quantize_append", "read_rows", "attend_rows",
+    "clip_rows", "quantize_rows", "quantize_rows_detail", "dequantize_rows", "pack_codes", "unpack_codes",
+    "PageFormat", "quantize_rotated", "quantize_append", "read_codes", "read_rows", "attend_rows",
     "attend", "attend_mixed", "attend_alg1", "residual_cov", "group_ranges", "effective_bpe",
     "clip_objectives", "calibrate_clip",
 ]
@@ -197,6 +197,14 @@ def clip_rows(Xr: np.ndarray, rho: float) -> np.ndarray:
 # Returns codes uint8 [..., d], s16, m16 float16 [..., d/G].
 # ----------------------------------------------------------------------------------
 def quantize_rows(Xc: np.ndarray, bits: int, G: int):
+    codes, s16, m16, _, _ = quantize_rows_detail(Xc, bits, G)
+    return codes, s16, m16
+
+
+def quantize_rows_detail(Xc: np.ndarray, bits: int, G: int):
+    """quantize_rows plus its intermediates: the fp32 scale s before the fp16 store [..., d/G] and
+    the exact pre-round value t = RN32(x - m16)·inv [..., d] (reading Z4), for checking that a
+    differing GPU code or metadata value sits on a rounding boundary."""
     Xc = np.asarray(Xc, dtype=np.float32)
     d = Xc.shape[-1]
     if d % G:
@@ -216,7 +224,7 @@ def quantize_rows(Xc: np.ndarray, bits: int, G: int):
     # rounded once, to the nearest integer (half-even) -- P:L1286-1295's real-arithmetic round
     t = dx.astype(np.float64) * inv.astype(np.float64)[..., None]
     c = np.clip(np.rint(t), 0, qmax).astype(np.uint8)               # np.rint = half-even
-    return c.reshape(Xc.shape), s16, m16
+    return c.reshape(Xc.shape), s16, m16, s, t.reshape(Xc.shape)
 
 
 # Q(x) = s (Q+ - z) = s16·c + m16, evaluated in fp64.
@@ -350,8 +358,9 @@ def quantize_append(K, V, slots, R_K, R_V, fmt: PageFormat, pool, rho_k=1.0, rho
     return quantize_rotated(rotate(K, R_K), rotate(V, R_V), slots, fmt, pool, rho_k, rho_v)
 
 
-def read_rows(pool: np.ndarray, slots, head: int, fmt: PageFormat):
-    """DequantHistory (Alg. 1 P:L1632) for one KV head: rotated-frame K̂r, V̂r [T, d] fp64."""
+def read_codes(pool: np.ndarray, slots, head: int, fmt: PageFormat):
+    """The stored codes and metadata of the given slots of one KV head: (K codes [T, d],
+    V codes [T, d], meta fp16 [T, d/G, 4] = (s_K, m_K, s_V, m_V))."""
     slots = np.asarray(slots, dtype=np.int64)
     T = slots.shape[0]
     rb = fmt.row_bytes
@@ -370,8 +379,14 @@ def read_rows(pool: np.ndarray, slots, head: int, fmt: PageFormat):
             meta[t, grp * 8: grp * 8 + 4] = blk[ko_: ko_ + 4]
             meta[t, grp * 8 + 4: grp * 8 + 8] = blk[vo_: vo_ + 4]
     m = meta.view(np.float16).reshape(T, ng, 4)
-    Kh = dequantize_rows(unpack_codes(pk, fmt.bits, fmt.d), m[..., 0], m[..., 1], fmt.G)
-    Vh = dequantize_rows(unpack_codes(pv, fmt.bits, fmt.d), m[..., 2], m[..., 3], fmt.G)
+    return unpack_codes(pk, fmt.bits, fmt.d), unpack_codes(pv, fmt.bits, fmt.d), m
+
+
+def read_rows(pool: np.ndarray, slots, head: int, fmt: PageFormat):
+    """DequantHistory (Alg. 1 P:L1632) for one KV head: rotated-frame K̂r, V̂r [T, d] fp64."""
+    ck, cv, m = read_codes(pool, slots, head, fmt)
+    Kh = dequantize_rows(ck, m[..., 0], m[..., 1], fmt.G)
+    Vh = dequantize_rows(cv, m[..., 2], m[..., 3], fmt.G)
     return Kh, Vh
 
 

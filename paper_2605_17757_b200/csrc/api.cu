@@ -3,6 +3,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdint>
 #include <new>
 #include <string>
 
@@ -13,14 +14,16 @@ cudaError_t launch_append_simple(const oscar_ctx& c, int mode, const void* K, co
                                  const float* Krot, const float* Vrot, const int64_t* slots,
                                  int64_t T, const float* RK, const float* RV, void* pool,
                                  float* rot_out, cudaStream_t s);
-cudaError_t launch_append_tc(const oscar_ctx& c, const void* K, const void* V,
-                             const int64_t* slots, int64_t T, const float* RK, const float* RV,
-                             void* pool, cudaStream_t s);
+cudaError_t launch_append_tc(const oscar_ctx& c, int mode, const void* K, const void* V, const float* xin_k,
+                             const float* xin_v, const int64_t* slots, int64_t T, const float* RK,
+                             const float* RV, void* pool, float* rot_out, cudaStream_t s);
 bool append_tc_supported(const oscar_ctx& c);
+bool append_tc_aligned(const void* K, const void* V);
 bool cov_tc_supported(const oscar_ctx& c);
 bool append_small_ok(const oscar_ctx& c, int64_t T);
-cudaError_t launch_append_small(const oscar_ctx& c, const void* K, const void* V, const int64_t* slots,
-                                int64_t T, const float* RK, const float* RV, void* pool, cudaStream_t s);
+cudaError_t launch_append_small(const oscar_ctx& c, int mode, const void* K, const void* V, const float* xin_k,
+                                const float* xin_v, const int64_t* slots, int64_t T, const float* RK,
+                                const float* RV, void* pool, float* rot_out, cudaStream_t s);
 cudaError_t launch_cov_accum_tc(const oscar_ctx& c, const void* Q, const void* SV, int64_t N, double* acc,
                                 cudaStream_t s);
 }  // namespace oscar
@@ -45,6 +48,36 @@ oscar_status cuda_status(cudaError_t e, const char* where) {
 }
 
 inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+// Which quantize_append kernel serves a call (the test hooks oscar_rotate / oscar_quantize_rotated
+// take the same route, so they isolate the stages of the kernel that produces the pool):
+//   variant 0: T <= 64 -> append_small_kernel (decode-size latency path); else the tensor-core
+//              append_tc_kernel when it applies (no clipping, 16-B aligned row bases);
+//   otherwise (variant 1, clipping, misaligned rows): append_simple_kernel.
+enum class AppendPath { kSmall, kTc, kSimple };
+AppendPath append_path(const oscar_ctx& c, int64_t T, const void* X0, const void* X1) {
+  if (c.variant != 0) return AppendPath::kSimple;
+  if (oscar::append_small_ok(c, T)) return AppendPath::kSmall;
+  if (oscar::append_tc_supported(c) && oscar::append_tc_aligned(X0, X1)) return AppendPath::kTc;
+  return AppendPath::kSimple;
+}
+
+cudaError_t launch_append(const oscar_ctx& c, int mode, const void* K, const void* V, const float* xin_k,
+                          const float* xin_v, const int64_t* slots, int64_t T, const float* RK,
+                          const float* RV, void* pool, float* rot_out, cudaStream_t s) {
+  const void* a = mode == 2 ? (const void*)xin_k : K;
+  const void* b = mode == 2 ? (const void*)xin_v : V;
+  switch (append_path(c, T, a, b)) {
+    case AppendPath::kSmall:
+      return oscar::launch_append_small(c, mode, K, V, xin_k, xin_v, slots, T, RK, RV, pool, rot_out, s);
+    case AppendPath::kTc:
+      return oscar::launch_append_tc(c, mode, K, V, xin_k, xin_v, slots, T, RK, RV, pool, rot_out, s);
+    default:
+      return oscar::launch_append_simple(c, mode, K, V, xin_k, xin_v, slots, T, RK, RV, pool, rot_out, s);
+  }
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 }  // namespace
 
 extern "C" {
@@ -121,7 +154,7 @@ oscar_status oscar_calib_accumulate(const oscar_ctx* ctx, const void* Q, const v
   if (N < 0) return fail(OSCAR_ERR_ARG, "N must be >= 0 (got %lld)", (long long)N);
   if (N == 0) return OSCAR_OK;
   if (!Q || !SV || !acc) return fail(OSCAR_ERR_ARG, "oscar_calib_accumulate: NULL pointer");
-  if (ctx->variant == 0 && oscar::cov_tc_supported(*ctx))
+  if (ctx->variant == 0 && oscar::cov_tc_supported(*ctx) && aligned16(Q) && aligned16(SV))
     return cuda_status(oscar::launch_cov_accum_tc(*ctx, Q, SV, N, acc, as_stream(stream)), "cov_accum_tc");
   return cuda_status(oscar::launch_cov_accum(*ctx, Q, SV, N, acc, as_stream(stream)), "cov_accum");
 }
@@ -188,13 +221,8 @@ oscar_status oscar_quantize_append(const oscar_ctx* ctx, const void* K, const vo
   if (T < 0) return fail(OSCAR_ERR_ARG, "T must be >= 0");
   if (T == 0) return OSCAR_OK;
   if (!K || !V || !slots || !R_K || !pool) return fail(OSCAR_ERR_ARG, "oscar_quantize_append: NULL pointer");
-  cudaStream_t s = as_stream(stream);
-  if (ctx->variant == 0 && oscar::append_small_ok(*ctx, T))      // decode-size: latency path
-    return cuda_status(oscar::launch_append_small(*ctx, K, V, slots, T, R_K, R_V, pool, s), "append_small");
-  if (ctx->variant == 0 && oscar::append_tc_supported(*ctx))
-    return cuda_status(oscar::launch_append_tc(*ctx, K, V, slots, T, R_K, R_V, pool, s), "append_tc");
-  return cuda_status(oscar::launch_append_simple(*ctx, 0, K, V, nullptr, nullptr, slots, T, R_K, R_V,
-                                                 pool, nullptr, s), "append_simple");
+  return cuda_status(launch_append(*ctx, 0, K, V, nullptr, nullptr, slots, T, R_K, R_V, pool, nullptr,
+                                   as_stream(stream)), "quantize_append");
 }
 
 oscar_status oscar_rotate(const oscar_ctx* ctx, const void* X, const float* R, float* Xrot,
@@ -203,9 +231,9 @@ oscar_status oscar_rotate(const oscar_ctx* ctx, const void* X, const float* R, f
   if (T < 0) return fail(OSCAR_ERR_ARG, "T must be >= 0");
   if (T == 0) return OSCAR_OK;
   if (!X || !R || !Xrot) return fail(OSCAR_ERR_ARG, "oscar_rotate: NULL pointer");
-  // the K half of the append kernel (blockIdx.z = 0) with output = fp32 rows
-  return cuda_status(oscar::launch_append_simple(*ctx, 1, X, X, nullptr, nullptr, nullptr, T, R, R,
-                                                 nullptr, Xrot, as_stream(stream)), "rotate");
+  // the K half of the kernel quantize_append would use, writing its fp32 rotated rows
+  return cuda_status(launch_append(*ctx, 1, X, X, nullptr, nullptr, nullptr, T, R, R, nullptr, Xrot,
+                                   as_stream(stream)), "rotate");
 }
 
 oscar_status oscar_quantize_rotated(const oscar_ctx* ctx, const float* Krot, const float* Vrot,
@@ -214,9 +242,8 @@ oscar_status oscar_quantize_rotated(const oscar_ctx* ctx, const float* Krot, con
   if (T < 0) return fail(OSCAR_ERR_ARG, "T must be >= 0");
   if (T == 0) return OSCAR_OK;
   if (!Krot || !Vrot || !slots || !pool) return fail(OSCAR_ERR_ARG, "oscar_quantize_rotated: NULL pointer");
-  return cuda_status(oscar::launch_append_simple(*ctx, 2, nullptr, nullptr, Krot, Vrot, slots, T, nullptr,
-                                                 nullptr, pool, nullptr, as_stream(stream)),
-                     "quantize_rotated");
+  return cuda_status(launch_append(*ctx, 2, nullptr, nullptr, Krot, Vrot, slots, T, nullptr, nullptr, pool,
+                                   nullptr, as_stream(stream)), "quantize_rotated");
 }
 
 size_t oscar_attend_workspace_bytes(const oscar_ctx* ctx, int32_t B, int32_t max_pages) {
@@ -240,6 +267,7 @@ oscar_status oscar_attend(const oscar_ctx* ctx, const void* q, const int32_t* pa
   const size_t need = oscar::attend_workspace_bytes(*ctx, B, max_pages);
   if (workspace_bytes < need)
     return fail(OSCAR_ERR_ARG, "workspace too small: %zu < %zu", workspace_bytes, need);
+  if (!aligned16(workspace)) return fail(OSCAR_ERR_ARG, "workspace must be 16-B (preferably 256-B) aligned");
   return cuda_status(oscar::launch_attend(*ctx, q, page_table, seq_lens, B, max_pages, pool, R_K, R_V,
                                           workspace, out, out_fp32, lse, as_stream(stream), nullptr,
                                           nullptr, nullptr, 0),
@@ -262,6 +290,7 @@ oscar_status oscar_decode_step(const oscar_ctx* ctx, const void* q, const void* 
   const size_t need = oscar::attend_workspace_bytes(*ctx, B, max_pages);
   if (workspace_bytes < need)
     return fail(OSCAR_ERR_ARG, "workspace too small: %zu < %zu", workspace_bytes, need);
+  if (!aligned16(workspace)) return fail(OSCAR_ERR_ARG, "workspace must be 16-B (preferably 256-B) aligned");
   return cuda_status(oscar::launch_attend(*ctx, q, page_table, seq_lens, B, max_pages, pool, R_K, R_V,
                                           workspace, out, out_fp32, lse, as_stream(stream), nullptr,
                                           nullptr, nullptr, 0, k_new, v_new),
@@ -288,6 +317,7 @@ oscar_status oscar_attend_mixed(const oscar_ctx* ctx, const void* q, const int32
   const size_t need = oscar::attend_workspace_bytes(*ctx, B, max_pages);
   if (workspace_bytes < need)
     return fail(OSCAR_ERR_ARG, "workspace too small: %zu < %zu", workspace_bytes, need);
+  if (!aligned16(workspace)) return fail(OSCAR_ERR_ARG, "workspace must be 16-B (preferably 256-B) aligned");
   return cuda_status(oscar::launch_attend(*ctx, q, page_table, seq_lens, B, max_pages, pool, R_K, R_V,
                                           workspace, out, out_fp32, lse, as_stream(stream), seg_k, seg_v,
                                           seg_lens, seg_cap),

@@ -1,7 +1,10 @@
 // quantize_append — Alg. 1 `Prefill` rotate-before-write + `QuantizeAndWrite`
 // (P:L1639-1643); §4 "KV Cache Update".  This file holds the simple reference
 // kernel (variant 1): rotation on CUDA cores in fp32, then clip / min-max / round / pack.
-// The tensor-core kernel (variant 0) lives in append_tc.cu and shares the epilogue below.
+// The decode-size kernel (append_small_kernel, below) and the decode step's prologue
+// (attend.cu) share its epilogue, quantize_store_row_warp (append_epilogue.cuh); the tensor-core
+// kernel (variant 0, append_tc.cu) has its own thread-per-token epilogue with the same reading-Z4
+// arithmetic, parity-tested through its own hooks.
 #include "common.cuh"
 #include "append_epilogue.cuh"
 
@@ -102,21 +105,32 @@ __global__ void __launch_bounds__(128) append_small_kernel(const uint16_t* __res
                                                            const int64_t* __restrict__ slots,
                                                            const float* __restrict__ RK,
                                                            const float* __restrict__ RV,
-                                                           uint8_t* __restrict__ pool, EpiParams ep) {
+                                                           uint8_t* __restrict__ pool, EpiParams ep,
+                                                           const float* __restrict__ xin_k,
+                                                           const float* __restrict__ xin_v,
+                                                           float* __restrict__ rot_out) {
   __shared__ __align__(16) float xs[kD];
   __shared__ __align__(16) float ys[kD];
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");   // PDL (see append_tc.cu)
   const int t = blockIdx.x, h = blockIdx.y, isV = blockIdx.z, c = threadIdx.x;
-  const uint16_t* X = isV ? V : K;
-  xs[c] = bf16_to_f32(X[((int64_t)t * ep.hkv + h) * kD + c]);
+  const int64_t row = (int64_t)t * ep.hkv + h;
+  const float* xin = isV ? xin_v : xin_k;  // quantize_rotated hook: given fp32 x̃, no rotation
+  if (!xin) {
+    const uint16_t* X = isV ? V : K;
+    xs[c] = bf16_to_f32(X[row * kD + c]);
+  }
   __syncthreads();
   const float* Rb = isV ? RV : RK;        // R_V = NULL: pre-rotated V (NEXT-2) -> identity
-  float acc = xs[c];
-  if (Rb) {
+  float acc = xin ? xin[row * kD + c] : xs[c];
+  if (Rb && !xin) {
     const float* R = Rb + (size_t)h * kD * kD + c;
     acc = 0.f;
 #pragma unroll 32
     for (int k = 0; k < kD; ++k) acc = fmaf(xs[k], R[(size_t)k * kD], acc);
+  }
+  if (rot_out) {                           // rotate hook: the fp32 x̃ the epilogue would quantize
+    rot_out[row * kD + c] = acc;
+    return;
   }
   ys[c] = acc;
   __syncthreads();
@@ -129,11 +143,15 @@ __global__ void __launch_bounds__(128) append_small_kernel(const uint16_t* __res
 
 bool append_small_ok(const oscar_ctx& c, int64_t T) { return T <= kSmallAppendMaxT; }
 
-cudaError_t launch_append_small(const oscar_ctx& c, const void* K, const void* V, const int64_t* slots,
-                                int64_t T, const float* RK, const float* RV, void* pool, cudaStream_t s) {
-  append_small_kernel<<<dim3((unsigned)T, c.hkv, 2), 128, 0, s>>>(
+// mode 0: quantize_append; mode 1: rotate hook (K = X, R_K = R -> rot_out, K half only);
+// mode 2: quantize_rotated hook (xin_k / xin_v fp32 rows, no rotation)
+cudaError_t launch_append_small(const oscar_ctx& c, int mode, const void* K, const void* V, const float* xin_k,
+                                const float* xin_v, const int64_t* slots, int64_t T, const float* RK,
+                                const float* RV, void* pool, float* rot_out, cudaStream_t s) {
+  append_small_kernel<<<dim3((unsigned)T, c.hkv, mode == 1 ? 1 : 2), 128, 0, s>>>(
       static_cast<const uint16_t*>(K), static_cast<const uint16_t*>(V), slots, RK, RV,
-      static_cast<uint8_t*>(pool), make_epi_params(c));
+      static_cast<uint8_t*>(pool), make_epi_params(c), mode == 2 ? xin_k : nullptr, mode == 2 ? xin_v : nullptr,
+      mode == 1 ? rot_out : nullptr);
   return cudaGetLastError();
 }
 

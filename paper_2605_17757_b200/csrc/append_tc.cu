@@ -16,12 +16,10 @@
 // Scope of this kernel: b in {2, 3, 4}, G in {32, 64, 128} (a G = 128 group spans the two channel
 // halves: the two warps swap min/max through smem), no clipping; other configs use the simple
 // kernel (append.cu).
-#include <cuda.h>
-#include <cudaTypedefs.h>
-
 #include <type_traits>
 
 #include "common.cuh"
+#include "ptx.cuh"
 
 namespace oscar {
 
@@ -46,61 +44,9 @@ struct TcSmem {
   uint32_t tmem_base;
 };
 
-__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(b)), "r"(n));
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  asm volatile(
-      "{\n.reg .pred p;\nW_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra W_%=;\n}\n" ::"r"(su32(b)), "r"(parity) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n"
-      ::"r"(su32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(su32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
-__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
-
-// UMMA shared-memory descriptor, K-major SWIZZLE_128B (8-row x 128-B atoms, SBO = 1024 B)
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
-  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
-         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
-}
+using namespace ptx;
 // instruction descriptor: kind::f16, A = B = BF16, D = F32, both K-major, M = 128, N = 128
-constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
-
-__device__ __forceinline__ void umma(uint32_t dt, uint64_t a, uint64_t b, uint32_t acc) {
-  asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n"
-      ::"r"(dt), "l"(a), "l"(b), "r"(kIdesc), "r"(acc));
-}
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(su32(bar))
-               : "memory");
-}
-
-#define OSCAR_LD32(base, v)                                                                          \
-  asm volatile(                                                                                       \
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15," \
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"                    \
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),           \
-        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),       \
-        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]),    \
-        "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]),    \
-        "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])                                             \
-      : "r"(base))
+constexpr uint32_t kIdesc = idesc_bf16(128, 128, false, false);
 
 struct TcParams {
   const int64_t* slots;
@@ -111,6 +57,10 @@ struct TcParams {
   int hkv, P, page_bytes, row_bytes, vcodes_off, meta_off, ng, G, bits;
   int cpp, tiles_per_pair;
   int lgP;                          // log2(P) if P is a power of two, else -1
+  // test hooks (MODE != 0): fp32 rotated rows in (MODE 2) / out (MODE 1), [T][hkv][128]
+  const float* xin_k;
+  const float* xin_v;
+  float* rot_out;
 };
 
 // Σ_i 0x4B400000 << (BITS·i) mod 2^32 over the codes of one 32-bit word: the constant part of
@@ -124,7 +74,12 @@ __device__ __forceinline__ constexpr uint32_t magic_words() {
 
 }  // namespace
 
-template <int BITS, int G>
+// MODE 0: production (TMA -> tcgen05 rotation -> quantize/pack/store epilogue).
+// MODE 1 (oscar_rotate hook): TMA -> tcgen05 rotation; the epilogue warps write the TMEM rows
+//        they would quantize as fp32 x̃ (K half only: one "pair" per head).
+// MODE 2 (oscar_quantize_rotated hook): no TMA / MMA; the epilogue warps take the given fp32 x̃
+//        rows in place of the TMEM load and run the identical quantize/pack/store code.
+template <int BITS, int G, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
 append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant__ CUtensorMap mapV, TcParams p) {
   extern __shared__ uint8_t smem_raw[];
@@ -134,7 +89,7 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
   // still starts after this kernel completes)
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   const int pair = blockIdx.x / p.cpp, sub = blockIdx.x % p.cpp;
-  const int h = pair >> 1, isV = pair & 1;
+  const int h = MODE == 1 ? pair : pair >> 1, isV = MODE == 1 ? 0 : pair & 1;
   const int ntiles = sub < p.tiles_per_pair ? (p.tiles_per_pair - sub + p.cpp - 1) / p.cpp : 0;
 
   // ---- R -> bf16 hi/lo, transposed to K-major (row n = output channel, k contiguous), SW128
@@ -166,10 +121,7 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
     for (int s = 0; s < kStages; ++s) { mbar_init(&S.full[s], 1); mbar_init(&S.empty[s], 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(&S.tfull[a], 1); mbar_init(&S.tempty[a], kEpiWarps / 2); }
   }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;\n" ::"r"(su32(&S.tmem_base)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
-  }
+  if (warp == 1) tmem_alloc(&S.tmem_base, 256);
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // B writes -> async proxy
   fence_before();
   __syncthreads();
@@ -178,7 +130,7 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
 
   if (warp == 0) {
     // ================= TMA producer
-    if (lane == 0) {
+    if (MODE != 2 && lane == 0) {
       const CUtensorMap* map = isV ? &mapV : &mapK;
       for (int i = 0; i < ntiles; ++i) {
         const int s = i % kStages;
@@ -191,7 +143,7 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
     }
   } else if (warp == 1) {
     // ================= MMA issuer
-    for (int i = 0; i < ntiles; ++i) {
+    for (int i = 0; i < (MODE == 2 ? 0 : ntiles); ++i) {
       const int s = i % kStages, a = i & 1;
       mbar_wait(&S.tempty[a], ((i >> 1) & 1) ^ 1);
       mbar_wait(&S.full[s], (i / kStages) & 1);
@@ -207,8 +159,8 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {
               const uint32_t ko = kc * (kTileBytes / 2) + kk * 32;
-              umma(dt, sw128_desc(abase + ko), sw128_desc(bbase + kc * (kBBytes / 2) + kk * 32),
-                   (part | kc | kk) != 0);
+              umma_f16<kIdesc>(dt, kmajor_sw128_desc(abase + ko),
+                               kmajor_sw128_desc(bbase + kc * (kBBytes / 2) + kk * 32), (part | kc | kk) != 0);
             }
         }
         umma_commit(&S.empty[s]);     // smem stage free once these MMAs complete
@@ -232,23 +184,47 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
     // slot of this thread's token, loaded one tile ahead (its latency is off the critical path)
     auto load_slot = [&](int i) -> int64_t {
       const int64_t tk = (int64_t)(sub + i * p.cpp) * kTok + r;
-      return (i < ntiles && tk < p.T) ? p.slots[tk] : -1;
+      return (MODE != 1 && i < ntiles && tk < p.T) ? p.slots[tk] : -1;
     };
     int64_t slot_next = load_slot(par);
     for (int i = par; i < ntiles; i += 2) {
       const int a = par;
       const int64_t slot = slot_next;
       slot_next = load_slot(i + 2);
-      mbar_wait(&S.tfull[a], (i >> 1) & 1);
-      fence_after();
       uint32_t v[64];
-      const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + a * 128 + half * 64;
-      OSCAR_LD32(taddr, v);
-      OSCAR_LD32(taddr + 32, (v + 32));
-      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-      fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&S.tempty[a]);
+      if constexpr (MODE != 2) {
+        mbar_wait(&S.tfull[a], (i >> 1) & 1);
+        fence_after();
+        const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + a * 128 + half * 64;
+        OSCAR_TMEM_LD32(taddr, v);
+        OSCAR_TMEM_LD32(taddr + 32, (v + 32));
+        tmem_ld_wait();
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.tempty[a]);
+      } else {
+        // hook: the given fp32 x̃ row (zeros past T) in place of the TMEM accumulator
+        const int64_t tk = (int64_t)(sub + i * p.cpp) * kTok + r;
+        const float* src = (isV ? p.xin_v : p.xin_k) + (tk * p.hkv + h) * kD + half * 64;
+#pragma unroll
+        for (int c4 = 0; c4 < 16; ++c4) {
+          const float4 f = tk < p.T ? reinterpret_cast<const float4*>(src)[c4] : make_float4(0.f, 0.f, 0.f, 0.f);
+          v[4 * c4] = __float_as_uint(f.x); v[4 * c4 + 1] = __float_as_uint(f.y);
+          v[4 * c4 + 2] = __float_as_uint(f.z); v[4 * c4 + 3] = __float_as_uint(f.w);
+        }
+      }
+      if constexpr (MODE == 1) {
+        // hook: the rotated row as the epilogue sees it (fp32 TMEM values)
+        const int64_t tk = (int64_t)(sub + i * p.cpp) * kTok + r;
+        if (tk < p.T) {
+          float4* dst = reinterpret_cast<float4*>(p.rot_out + (tk * p.hkv + h) * kD + half * 64);
+#pragma unroll
+          for (int c4 = 0; c4 < 16; ++c4)
+            dst[c4] = make_float4(__uint_as_float(v[4 * c4]), __uint_as_float(v[4 * c4 + 1]),
+                                  __uint_as_float(v[4 * c4 + 2]), __uint_as_float(v[4 * c4 + 3]));
+        }
+        continue;
+      }
 
       const bool valid = slot >= 0;
       // V fast path: the quarter's 32 tokens go to 32 consecutive slots starting on a 16-token
@@ -391,71 +367,60 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
   __syncthreads();
   if (warp == 1) {
     fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;\n" ::"r"(tmem));
+    tmem_dealloc(tmem, 256);
   }
 }
 
 // ---------------------------------------------------------------- host side
 namespace {
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
-    void* ptr = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
-  }
-  return fn;
-}
-
+// K or V [T][hkv][128] bf16: box {64 channels, 1 head, 128 tokens}
 bool make_map(CUtensorMap* m, const void* base, int64_t T, int hkv) {
-  auto fn = encode_fn();
-  if (!fn) return false;
-  cuuint64_t dims[3] = {(cuuint64_t)kD, (cuuint64_t)hkv, (cuuint64_t)T};
-  cuuint64_t strides[2] = {(cuuint64_t)kD * 2, (cuuint64_t)hkv * kD * 2};
-  cuuint32_t box[3] = {64, 1, (cuuint32_t)kTok};
-  cuuint32_t estr[3] = {1, 1, 1};
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  return ptx::make_bf16_map_3d(m, base, T, hkv, 1, kTok);
 }
 
 using TcFn = void (*)(CUtensorMap, CUtensorMap, TcParams);
+template <int MODE>
 TcFn pick(int bits, int G) {
-  if (bits == 2 && G == 64) return append_tc_kernel<2, 64>;
-  if (bits == 2 && G == 32) return append_tc_kernel<2, 32>;
-  if (bits == 4 && G == 64) return append_tc_kernel<4, 64>;
-  if (bits == 4 && G == 32) return append_tc_kernel<4, 32>;
-  if (bits == 2 && G == 128) return append_tc_kernel<2, 128>;
-  if (bits == 3 && G == 32) return append_tc_kernel<3, 32>;
-  if (bits == 3 && G == 64) return append_tc_kernel<3, 64>;
-  if (bits == 3 && G == 128) return append_tc_kernel<3, 128>;
-  if (bits == 4 && G == 128) return append_tc_kernel<4, 128>;
+#define OSCAR_TC(B_, G_) if (bits == B_ && G == G_) return append_tc_kernel<B_, G_, MODE>;
+  OSCAR_TC(2, 32) OSCAR_TC(2, 64) OSCAR_TC(2, 128)
+  OSCAR_TC(3, 32) OSCAR_TC(3, 64) OSCAR_TC(3, 128)
+  OSCAR_TC(4, 32) OSCAR_TC(4, 64) OSCAR_TC(4, 128)
+#undef OSCAR_TC
   return nullptr;
 }
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 }  // namespace
 
+// The tensor-core kernel covers every (b, G) without clipping; TMA needs 16-B aligned row bases
+// (callers fall back to the simple kernel otherwise, api.cu).
 bool append_tc_supported(const oscar_ctx& c) {
-  return c.d == 128 && c.clip_k_idx < 0 && c.clip_v_idx < 0 && pick(c.bits, c.G) != nullptr &&
-         encode_fn() != nullptr;
+  return c.d == 128 && c.clip_k_idx < 0 && c.clip_v_idx < 0 && pick<0>(c.bits, c.G) != nullptr &&
+         ptx::encode_tiled_fn() != nullptr;
 }
+bool append_tc_aligned(const void* K, const void* V) { return aligned16(K) && aligned16(V); }
 
-cudaError_t launch_append_tc(const oscar_ctx& c, const void* K, const void* V, const int64_t* slots,
-                             int64_t T, const float* RK, const float* RV, void* pool, cudaStream_t s) {
-  TcFn fn = pick(c.bits, c.G);
+// mode 0: quantize_append(K, V); mode 1: rotate hook (K = X, R_K = R, fp32 rows to rot_out);
+// mode 2: quantize_rotated hook (xin_k, xin_v fp32 rows, no rotation)
+cudaError_t launch_append_tc(const oscar_ctx& c, int mode, const void* K, const void* V, const float* xin_k,
+                             const float* xin_v, const int64_t* slots, int64_t T, const float* RK,
+                             const float* RV, void* pool, float* rot_out, cudaStream_t s) {
+  TcFn fn = mode == 0 ? pick<0>(c.bits, c.G) : mode == 1 ? pick<1>(c.bits, c.G) : pick<2>(c.bits, c.G);
   if (!fn) return cudaErrorNotSupported;
-  if ((reinterpret_cast<uintptr_t>(K) | reinterpret_cast<uintptr_t>(V)) & 15) return cudaErrorMisalignedAddress;
-  CUtensorMap mk, mv;
-  if (!make_map(&mk, K, T, c.hkv) || !make_map(&mv, V, T, c.hkv)) return cudaErrorInvalidValue;
+  CUtensorMap mk{}, mv{};
+  if (mode != 2) {
+    if (!aligned16(K) || !aligned16(V)) return cudaErrorMisalignedAddress;
+    if (!make_map(&mk, K, T, c.hkv) || !make_map(&mv, V, T, c.hkv)) return cudaErrorInvalidValue;
+  }
   TcParams p{};
   p.slots = slots; p.T = T; p.RK = RK; p.RV = RV; p.pool = static_cast<uint8_t*>(pool);
   p.hkv = c.hkv; p.P = c.P; p.page_bytes = c.page_bytes; p.row_bytes = c.row_bytes;
   p.vcodes_off = c.vcodes_off; p.meta_off = c.meta_off; p.ng = c.ng; p.G = c.G; p.bits = c.bits;
+  p.xin_k = xin_k; p.xin_v = xin_v; p.rot_out = rot_out;
   p.lgP = -1;
   for (int k = 0; k < 16; ++k)
     if ((1 << k) == c.P) p.lgP = k;
-  const int pairs = 2 * c.hkv;
+  const int pairs = mode == 1 ? c.hkv : 2 * c.hkv;
   p.tiles_per_pair = (int)((T + kTok - 1) / kTok);
   int cpp = c.num_sms / pairs;
   if (cpp < 1) cpp = 1;

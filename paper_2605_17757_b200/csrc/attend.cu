@@ -667,13 +667,41 @@ static int choose_pps(const oscar_ctx& c, int B, int max_pages) {
   return (int)(pps < lo ? lo : pps);
 }
 
-size_t attend_workspace_bytes(const oscar_ctx& c, int B, int max_pages) {
+// Workspace carve-up: every sub-buffer starts on a 256-B boundary (the kernels use 8- and 16-B
+// vector accesses on them, and B·H_q may be odd).
+struct WsLayout {
+  size_t qt, ws_o, ws_m, ws_l, qsum, qscale, qint, qfrag, work, seg_o, seg_m, seg_l, total;
+};
+static WsLayout ws_layout(const oscar_ctx& c, int B, int max_pages) {
   const int pps = choose_pps(c, B, max_pages);
   const size_t ns = (size_t)((max_pages + pps - 1) / pps);
   const size_t rows = (size_t)B * c.hq;
   const size_t nt = (size_t)((c.g * c.ng + 7) / 8);
-  return rows * kD * 4 + rows * ns * (kD + 2) * 4 + rows * (kD * 2 + 4 + 32) +
-         (size_t)B * c.hkv * nt * 16 * 32 * 4 + rows * (kD + 2) * 4 + 1024;
+  WsLayout w{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off = (off + bytes + 255) / 256 * 256;
+    return o;
+  };
+  w.qt = take(rows * kD * 4);
+  w.ws_o = take(rows * ns * kD * 4);
+  w.ws_m = take(rows * ns * 4);
+  w.ws_l = take(rows * ns * 4);
+  w.qsum = take(rows * 8 * 4);
+  w.qscale = take(rows * 4);
+  w.qint = take(rows * kD * 2);
+  w.qfrag = take((size_t)B * c.hkv * nt * 16 * 32 * 4);
+  w.work = take(64 * 4);
+  w.seg_o = take(rows * kD * 4);
+  w.seg_m = take(rows * 4);
+  w.seg_l = take(rows * 4);
+  w.total = off;
+  return w;
+}
+
+size_t attend_workspace_bytes(const oscar_ctx& c, int B, int max_pages) {
+  return ws_layout(c, B, max_pages).total;
 }
 
 cudaError_t launch_attend_mma(const AttnParams& p, int total_warps, cudaStream_t s);
@@ -695,21 +723,24 @@ cudaError_t launch_attend(const oscar_ctx& c, const void* q, const int32_t* page
   p.nt = (c.g * c.ng + 7) / 8;
   p.n_items = B * c.hkv * p.n_splits;
   p.batch = B;
-  // workspace carve-up (attend_workspace_bytes)
-  const size_t rows = (size_t)B * c.hq;
-  p.qt = static_cast<float*>(ws);
-  p.ws_o = p.qt + rows * kD;
-  p.ws_m = p.ws_o + rows * p.n_splits * kD;
-  p.ws_l = p.ws_m + rows * p.n_splits;
-  p.qsum = reinterpret_cast<int32_t*>(p.ws_l + rows * p.n_splits);
-  p.qscale = reinterpret_cast<float*>(p.qsum + rows * 8);
-  p.qint = reinterpret_cast<int16_t*>(p.qscale + rows);
-  p.qfrag = reinterpret_cast<uint32_t*>(p.qint + rows * kD);
-  p.work = reinterpret_cast<int32_t*>(p.qfrag + (size_t)B * c.hkv * p.nt * 16 * 32);
-  if (seg_k) {
-    p.seg_o = reinterpret_cast<float*>(p.work + 64);
-    p.seg_m = p.seg_o + rows * kD;
-    p.seg_l = p.seg_m + rows;
+  // workspace carve-up (ws_layout: 256-B aligned sub-buffers)
+  {
+    const WsLayout w = ws_layout(c, B, max_pages);
+    uint8_t* base = static_cast<uint8_t*>(ws);
+    p.qt = reinterpret_cast<float*>(base + w.qt);
+    p.ws_o = reinterpret_cast<float*>(base + w.ws_o);
+    p.ws_m = reinterpret_cast<float*>(base + w.ws_m);
+    p.ws_l = reinterpret_cast<float*>(base + w.ws_l);
+    p.qsum = reinterpret_cast<int32_t*>(base + w.qsum);
+    p.qscale = reinterpret_cast<float*>(base + w.qscale);
+    p.qint = reinterpret_cast<int16_t*>(base + w.qint);
+    p.qfrag = reinterpret_cast<uint32_t*>(base + w.qfrag);
+    p.work = reinterpret_cast<int32_t*>(base + w.work);
+    if (seg_k) {
+      p.seg_o = reinterpret_cast<float*>(base + w.seg_o);
+      p.seg_m = reinterpret_cast<float*>(base + w.seg_m);
+      p.seg_l = reinterpret_cast<float*>(base + w.seg_l);
+    }
   }
 
   cudaLaunchAttribute pdl[1];

@@ -26,6 +26,7 @@
 #include <type_traits>
 
 #include "attend_common.cuh"
+#include "ptx.cuh"
 
 namespace oscar {
 
@@ -127,36 +128,10 @@ __device__ __forceinline__ void halves_f2(uint32_t w0, uint32_t w1, f2& lo, f2& 
   hi = f2{__high2float(a), __high2float(b)};
 }
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
-                                          uint64_t policy) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
-      : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(phase)
-      : "memory");
-}
+using ptx::mbar_init;
+using ptx::mbar_wait;
+using ptx::bulk_load;
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return ptx::su32(p); }
 
 // PV M-tile row -> channel: row gid of M-tile i (+64 for rows gid+8); CPB codes per byte
 template <int BITS>

@@ -9,10 +9,8 @@
 // Each work unit accumulates kRowsPerUnit rows in fp32 TMEM (reading H4: bounded fp32 chunk)
 // and is then flushed with fp64 red.add into acc[h][which][128][128]; two TMEM accumulators
 // let the next unit's MMAs overlap the flush.
-#include <cuda.h>
-#include <cudaTypedefs.h>
-
 #include "common.cuh"
+#include "ptx.cuh"
 
 namespace oscar {
 
@@ -31,62 +29,9 @@ struct CovSmem {
   uint32_t tmem_base;
 };
 
-__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(b)), "r"(n));
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  asm volatile(
-      "{\n.reg .pred p;\nW_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra W_%=;\n}\n" ::"r"(su32(b)), "r"(parity) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n"
-      ::"r"(su32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(su32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
-__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
-
-// MN-major SWIZZLE_128B descriptor: 64 elements (128 B) contiguous along M/N per row, rows =
-// K; LBO = byte stride between the two 64-channel blocks, SBO = 1024 B between 8-row groups.
-__device__ __forceinline__ uint64_t mn_sw128_desc(uint32_t saddr, uint32_t lbo) {
-  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
-         ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
-}
+using namespace ptx;
 // kind::f16, A = B = BF16, D = F32, A and B MN-major, M = 128, N = 128
-constexpr uint32_t kIdescCov = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (1u << 16) |
-                               ((128u >> 3) << 17) | ((128u >> 4) << 24);
-
-__device__ __forceinline__ void umma(uint32_t dt, uint64_t a, uint64_t b, uint32_t acc) {
-  asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n"
-      ::"r"(dt), "l"(a), "l"(b), "r"(kIdescCov), "r"(acc));
-}
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(su32(bar))
-               : "memory");
-}
-
-#define OSCAR_CLD32(base, v)                                                                         \
-  asm volatile(                                                                                       \
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15," \
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"                    \
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),           \
-        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),       \
-        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]),    \
-        "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]),    \
-        "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])                                             \
-      : "r"(base))
+constexpr uint32_t kIdescCov = idesc_bf16(128, 128, true, true);
 
 struct CovParams {
   double* acc;             // [H_kv][2][128][128]
@@ -114,11 +59,10 @@ cov_accum_tc_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_const
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStagesC; ++s) { mbar_init(&S.full[s], 1); mbar_init(&S.empty[s], 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(&S.tfull[a], 1); mbar_init(&S.tempty[a], 4); }
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    mbar_init_fence();
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;\n" ::"r"(su32(&S.tmem_base)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    tmem_alloc(&S.tmem_base, 256);
   }
   fence_before();
   __syncthreads();
@@ -162,8 +106,8 @@ cov_accum_tc_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_const
           const uint32_t base = su32(S.A[s]);
 #pragma unroll
           for (int kk = 0; kk < kRows / 16; ++kk) {
-            const uint64_t d = mn_sw128_desc(base + kk * 2048, kTileB / 2);
-            umma(tmem + a * 128, d, d, (i | kk) != 0);
+            const uint64_t d = mnmajor_sw128_desc(base + kk * 2048, kTileB / 2);
+            umma_f16<kIdescCov>(tmem + a * 128, d, d, (i | kk) != 0);
           }
           umma_commit(&S.empty[s]);
         }
@@ -185,8 +129,8 @@ cov_accum_tc_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_const
 #pragma unroll 1
       for (int c0 = 0; c0 < kD; c0 += 32) {
         uint32_t v[32];
-        OSCAR_CLD32(tmem + ((uint32_t)(quarter * 32) << 16) + a * 128 + c0, v);
-        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        OSCAR_TMEM_LD32(tmem + ((uint32_t)(quarter * 32) << 16) + a * 128 + c0, v);
+        tmem_ld_wait();
 #pragma unroll
         for (int j = 0; j < 32; ++j) S.accd[(c0 + j) * kD + i] += (double)__uint_as_float(v[j]);
       }
@@ -204,39 +148,20 @@ cov_accum_tc_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_const
   __syncthreads();
   if (warp == 1) {
     fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;\n" ::"r"(tmem));
+    tmem_dealloc(tmem, 256);
   }
 }
 
 // ---------------------------------------------------------------- host side
 namespace {
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn_c() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
-    void* ptr = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
-  }
-  return fn;
-}
-
+// rows r = token·g + i_g of KV head h: box {64 channels, g heads, 128/g tokens}
 bool make_cov_map(CUtensorMap* m, const void* base, int64_t N, int hq, int g) {
-  auto fn = encode_fn_c();
-  if (!fn) return false;
-  cuuint64_t dims[3] = {(cuuint64_t)kD, (cuuint64_t)hq, (cuuint64_t)N};
-  cuuint64_t strides[2] = {(cuuint64_t)kD * 2, (cuuint64_t)hq * kD * 2};
-  cuuint32_t box[3] = {64, (cuuint32_t)g, (cuuint32_t)(kRows / g)};
-  cuuint32_t estr[3] = {1, 1, 1};
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  return ptx::make_bf16_map_3d(m, base, N, hq, g, kRows / g);
 }
 }  // namespace
 
 bool cov_tc_supported(const oscar_ctx& c) {
-  return c.d == 128 && (128 % c.g) == 0 && encode_fn_c() != nullptr;
+  return c.d == 128 && (128 % c.g) == 0 && ptx::encode_tiled_fn() != nullptr;
 }
 
 cudaError_t launch_cov_accum_tc(const oscar_ctx& c, const void* Q, const void* SV, int64_t N, double* acc,

@@ -2,8 +2,9 @@
 inputs.  Tolerances (north star):
   * rotated values: per row max|Δ| / ‖x̃‖₂ <= 1e-5                     (reading Z26)
   * codes / metadata / pool bytes: bit-exact given identical rotated inputs
-  * full append: bit-exact except rounding-boundary flips (|Δcode| = 1 where the oracle's
-    pre-round value is within 1e-4 of a .5 boundary, or fp16 metadata 1 ulp apart)
+  * full append: bit-exact except rounding-boundary flips, every one validated
+    (oracle/boundary.py: |Δcode| = 1 with the oracle's pre-round value within the 1e-5 rotation
+    bound of .5, or fp16 metadata one ulp apart at a rounding midpoint)
   * attention: fp32-output mode <= 2e-3 max-abs vs the fp64 oracle; bf16 mode ==
     RNE(fp32 mode) bit-for-bit (reading Z25)
 """
@@ -34,16 +35,26 @@ def make(**kw):
     return B.Oscar(B.Config(**kw))
 
 
+ALL_BG = [(b, g) for b in (2, 3, 4) for g in (32, 64, 128)]
+
+
 # ---------------------------------------------------------------------------- rotation
-@pytest.mark.parametrize("T_", [1, 33, 300])
-def test_rotate_parity(T_):
+# oscar_rotate takes the route oscar_quantize_append takes for the same T and config (api.cu
+# append_path): T <= 64 -> append_small_kernel, else the tcgen05 append_tc_kernel (MODE 1: its
+# TMEM rows dumped as fp32), variant 1 -> the simple kernel.  Every <b, G> instance of the
+# tensor-core kernel is checked (the rotation is shared, the instances differ in the epilogue).
+@pytest.mark.parametrize("bits,G", ALL_BG)
+@pytest.mark.parametrize("T_", [33, 300])
+@pytest.mark.parametrize("variant", [0, 1])
+def test_rotate_parity(bits, G, T_, variant):
     torch = _torch()
-    rng = np.random.default_rng(100 + T_)
+    rng = np.random.default_rng(100 + T_ + bits * 7 + G)
     H = 3
     X = synth.gen_keys(rng, T_, H, 128)
     R = synth.gen_rotation(rng, H, 128)
-    o = make(num_q_heads=H, num_kv_heads=H)
-    out = torch.empty((T_, H, 128), dtype=torch.float32, device="cuda")
+    o = make(num_q_heads=H, num_kv_heads=H, bits=bits, group_size=G)
+    o.set_variant(variant)
+    out = torch.full((T_, H, 128), float("nan"), dtype=torch.float32, device="cuda")
     o.rotate(T(X, torch.bfloat16), T(R), out)
     ref = O.rotate(X, R).astype(np.float64)
     got = out.cpu().numpy().astype(np.float64)
@@ -62,21 +73,31 @@ def _adversarial_rows(rng, n, H):
     return X
 
 
-@pytest.mark.parametrize("bits,G,rho", [(2, 64, (1.0, 1.0)), (2, 32, (0.96, 0.92)),
-                                        (4, 32, (1.0, 1.0)), (4, 128, (0.96, 0.92)),
-                                        (2, 128, (0.5, 0.999))])
-def test_quantize_rotated_bit_exact(bits, G, rho):
+# oscar_quantize_rotated ("identical rotated inputs"): the route of quantize_append for that T —
+# T = 333: the tcgen05 kernel's epilogue (MODE 2, no clipping) / the simple kernel (clipping,
+# variant 1); T = 40: append_small_kernel's epilogue.  Bit-exact pool bytes.
+@pytest.mark.parametrize("bits,G,rho", [(b, g, (1.0, 1.0)) for b, g in ALL_BG] + [
+    (2, 32, (0.96, 0.92)), (4, 128, (0.96, 0.92)), (2, 128, (0.5, 0.999)), (3, 64, (0.96, 0.92))])
+@pytest.mark.parametrize("Tn", [333, 40])
+@pytest.mark.parametrize("variant", [0, 1])
+def test_quantize_rotated_bit_exact(bits, G, rho, Tn, variant):
     torch = _torch()
-    rng = np.random.default_rng(bits * 1000 + G)
-    H, Tn, npages = 2, 333, 8
+    rng = np.random.default_rng(bits * 1000 + G + Tn)
+    H, npages = 2, 8
     fmt = O.PageFormat(128, bits, G, 64)
     Kr = _adversarial_rows(rng, Tn, H)
     Vr = _adversarial_rows(rng, Tn, H)[::-1].copy()
     slots = rng.permutation(npages * 64)[:Tn].astype(np.int64)
+    if Tn == 333:                                    # a 16-aligned run: the staged-V 16-B store path
+        slots[100:164] = np.arange(320, 384)
+        rest = np.setdiff1d(np.arange(npages * 64), slots[100:164])
+        others = np.concatenate([np.arange(100), np.arange(164, Tn)])
+        slots[others] = rng.permutation(rest)[:len(others)]
     ref = np.zeros((npages, H, fmt.page_bytes), np.uint8)
     O.quantize_rotated(Kr, Vr, slots, fmt, ref, rho[0], rho[1])
     o = make(num_q_heads=H, num_kv_heads=H, bits=bits, group_size=G, clip_ratio_k=rho[0],
              clip_ratio_v=rho[1])
+    o.set_variant(variant)
     pool = torch.zeros((npages, H, o.page_bytes()), dtype=torch.uint8, device="cuda")
     o.quantize_rotated(T(Kr), T(Vr), T(slots), pool)
     got = pool.cpu().numpy()
@@ -85,14 +106,6 @@ def test_quantize_rotated_bit_exact(bits, G, rho):
 
 
 # ---------------------------------------------------------------------------- full append
-def _decode_pool(pool, slots, H, fmt):
-    out = []
-    for h in range(H):
-        Kh, Vh = O.read_rows(pool, slots, h, fmt)
-        out.append((Kh, Vh))
-    return out
-
-
 def _slots(rng, mode, Tn, npages):
     """perm: random distinct slots.  contigN: the first 700 tokens take consecutive slots from
     slot N (a 16-aligned N exercises the tensor-core kernel's staged V path, also across page
@@ -103,6 +116,15 @@ def _slots(rng, mode, Tn, npages):
     run = np.arange(start, start + 700)
     rest = np.setdiff1d(np.arange(npages * 64), run)
     return np.concatenate([run, rng.permutation(rest)[:Tn - 700]]).astype(np.int64)
+
+
+def check_append_flips(got, K, V, RK, RV, slots, fmt, rho=(1.0, 1.0)):
+    """Every byte that differs from the oracle's pool must be a rounding-boundary flip of the
+    fp32 rotation (oracle/boundary.py: codes |Δ| = 1 with the oracle's pre-round value within the
+    1e-5 rotation bound of .5, or fp16 metadata one ulp apart at a rounding midpoint)."""
+    from oracle.boundary import check_pool_flips
+    rot = {"K": O.rotate(K, RK), "V": O.rotate(V, RV)}
+    return check_pool_flips(got, rot, slots, fmt, rho)
 
 
 @pytest.mark.parametrize("bits,G,rho,variant,Tn,slot_mode", [
@@ -135,19 +157,16 @@ def test_quantize_append_parity(bits, G, rho, variant, Tn, slot_mode):
     pool = torch.zeros((npages, H, o.page_bytes()), dtype=torch.uint8, device="cuda")
     o.quantize_append(T(K, torch.bfloat16), T(V, torch.bfloat16), T(slots), T(RK), T(RV), pool)
     got = pool.cpu().numpy()
-    nbad = int((got != ref).sum())
-    frac = nbad / got.size
-    # bytes differ only at rounding-boundary flips; dequantized rows agree within one step
-    assert frac < 2e-4, frac
-    rot = {"K": O.rotate(K, RK), "V": O.rotate(V, RV)}
-    for h, ((Kg, Vg), (Ko, Vo)) in enumerate(zip(_decode_pool(got, slots, H, fmt), _decode_pool(ref, slots, H, fmt))):
-        for name, g_, r_ in [("K", Kg, Ko), ("V", Vg, Vo)]:
-            x = rot[name][:, h].astype(np.float64)
-            step = np.abs(x).max() / 2 ** bits * 4
-            assert np.abs(g_ - r_).max() <= step, (name, h)
+    # every written byte equals the oracle's up to validated boundary flips; untouched slots stay 0
+    st = check_append_flips(got, K, V, RK, RV, slots, fmt, rho)
+    free = np.setdiff1d(np.arange(npages * 64), slots)
+    for h in range(H):
+        ck, cv, m = O.read_codes(got, free, h, fmt)
+        assert not ck.any() and not cv.any() and not m.view(np.uint16).any()
+    assert st["code_flips"] + st["meta_flips"] <= 1e-3 * st["groups"] * G, st
 
 
-@pytest.mark.parametrize("P,bits,G", [(16, 2, 64), (256, 2, 128), (32, 4, 32), (128, 4, 64)])
+@pytest.mark.parametrize("P,bits,G", [(16, 2, 64), (256, 2, 128), (32, 4, 32), (128, 4, 64), (48, 3, 32)])
 def test_quantize_append_page_sizes(P, bits, G):
     """Other page sizes through the default (tensor-core where supported) append: 700 tokens in
     consecutive slots from a 16-aligned start (staged V path) plus random slots."""
@@ -166,8 +185,28 @@ def test_quantize_append_page_sizes(P, bits, G):
     o = make(num_q_heads=H * 4, num_kv_heads=H, bits=bits, group_size=G, page_size=P)
     pool = torch.zeros((npages, H, o.page_bytes()), dtype=torch.uint8, device="cuda")
     o.quantize_append(T(K, torch.bfloat16), T(V, torch.bfloat16), T(slots), T(RK), T(RV), pool)
-    got = pool.cpu().numpy()
-    assert (got != ref).sum() / got.size < 2e-4
+    check_append_flips(pool.cpu().numpy(), K, V, RK, RV, slots, fmt)
+
+
+def test_quantize_append_misaligned_falls_back():
+    """Row bases that are not 16-B aligned (TMA cannot take them) route to the simple kernel
+    instead of failing; the result is the same pool up to boundary flips."""
+    torch = _torch()
+    rng = np.random.default_rng(77)
+    H, Tn, npages = 2, 300, 8
+    fmt = O.PageFormat(128, 2, 64, 64)
+    K, V = synth.gen_keys(rng, Tn, H, 128), synth.gen_values(rng, Tn, H, 128)
+    RK, RV = synth.gen_rotation(rng, H, 128), synth.gen_rotation(rng, H, 128)
+    slots = rng.permutation(npages * 64)[:Tn].astype(np.int64)
+    o = make(num_q_heads=H, num_kv_heads=H)
+    kb = torch.zeros(Tn * H * 128 + 1, dtype=torch.bfloat16, device="cuda")
+    vb = torch.zeros_like(kb)
+    kb[1:] = T(K, torch.bfloat16).reshape(-1)
+    vb[1:] = T(V, torch.bfloat16).reshape(-1)
+    Km, Vm = kb[1:].view(Tn, H, 128), vb[1:].view(Tn, H, 128)     # 2-byte offset: misaligned
+    pool = torch.zeros((npages, H, o.page_bytes()), dtype=torch.uint8, device="cuda")
+    o.quantize_append(Km, Vm, T(slots), T(RK), T(RV), pool)
+    check_append_flips(pool.cpu().numpy(), K, V, RK, RV, slots, fmt)
 
 
 # ---------------------------------------------------------------------------- attention
@@ -210,17 +249,21 @@ def _run_attend(o, q, pt, L, pool, RK, RV):
     dict(name="g4G32", Hq=8, Hkv=2, bits=4, G=32, B=2, L=[450, 64]),        # 4 groups x 4 heads
     dict(name="b3", Hq=8, Hkv=2, bits=3, G=64, B=2, L=[333, 64]),           # 3-bit: simple kernels
     dict(name="C2G32", Hq=32, Hkv=8, bits=2, G=32, B=3, L=[1000, 77, 0]),   # token-row layout, 4 groups
+    dict(name="b3G32", Hq=8, Hkv=2, bits=3, G=32, B=2, L=[290, 17]),
+    dict(name="b3G128", Hq=16, Hkv=2, bits=3, G=128, B=2, L=[300, 64]),
+    dict(name="b4g8", Hq=16, Hkv=2, bits=4, G=64, B=2, L=[250, 1]),
 ])
 @pytest.mark.parametrize("variant", [0, 1])
 @pytest.mark.parametrize("pps", [0, 1, 3])
-def test_attend_parity(cfg, variant, pps):
+@pytest.mark.parametrize("qsig", [2.0, 8.0])          # 8.0: the "peaky" decode q
+def test_attend_parity(cfg, variant, pps, qsig):
     torch = _torch()
     rng = np.random.default_rng(hash(cfg["name"]) % 2 ** 31)
     fmt = O.PageFormat(128, cfg["bits"], cfg["G"], 64)
     L = list(range(4, 260, 4)) if cfg["L"] == "ramp256" else cfg["L"]
     B = cfg["B"]
     pt, pool, RK, RV = _oracle_pool(rng, fmt, B, cfg["Hkv"], L)
-    q = synth.gen_decode_q(rng, B, cfg["Hq"], 128)
+    q = synth.gen_decode_q(rng, B, cfg["Hq"], 128, sigma=qsig)
     ref, ref_lse = O.attend(q, pt, L, pool, RK, RV, fmt, cfg["Hkv"])
     o = make(num_q_heads=cfg["Hq"], num_kv_heads=cfg["Hkv"], bits=cfg["bits"], group_size=cfg["G"],
              attend_pages_per_split=pps)
@@ -238,10 +281,13 @@ def test_attend_parity(cfg, variant, pps):
 
 
 @pytest.mark.parametrize("P,bits,G,Hq,Hkv", [(32, 2, 64, 32, 8), (128, 2, 64, 32, 8), (16, 2, 128, 16, 2),
-                                            (256, 4, 64, 8, 2), (32, 4, 32, 8, 2)])
-def test_attend_page_sizes(P, bits, G, Hq, Hkv):
+                                            (256, 4, 64, 8, 2), (32, 4, 32, 8, 2), (48, 2, 64, 32, 8),
+                                            (48, 3, 64, 8, 2), (256, 3, 128, 8, 2), (80, 3, 32, 4, 1)])
+@pytest.mark.parametrize("variant", [0, 1])
+def test_attend_page_sizes(P, bits, G, Hq, Hkv, variant):
     """Page sizes other than 64 (the FULL-page fast path never applies): tensor-core kernels'
-    generic masked path against the oracle, ragged lengths."""
+    generic masked path against the oracle, ragged lengths; P that does not divide 128 takes the
+    simple kernel's one-(token, head)-per-thread scoring path."""
     torch = _torch()
     rng = np.random.default_rng(P * 7 + bits + G)
     fmt = O.PageFormat(128, bits, G, P)
@@ -250,8 +296,54 @@ def test_attend_page_sizes(P, bits, G, Hq, Hkv):
     q = synth.gen_decode_q(rng, len(L), Hq, 128)
     ref, _ = O.attend(q, pt, L, pool, RK, RV, fmt, Hkv)
     o = make(num_q_heads=Hq, num_kv_heads=Hkv, bits=bits, group_size=G, page_size=P)
+    o.set_variant(variant)
     out32, out16, _ = _run_attend(o, q, pt, L, pool, RK, RV)
     assert np.abs(out32.cpu().numpy().astype(np.float64) - ref).max() <= 2e-3
+
+
+@pytest.mark.parametrize("B,Hq,Hkv", [(1, 1, 1), (3, 1, 1), (1, 2, 1), (2, 1, 1), (3, 2, 2), (5, 4, 4)])
+@pytest.mark.parametrize("call", ["attend", "decode_step", "attend_mixed"])
+def test_attend_odd_row_counts(B, Hq, Hkv, call):
+    """B·H_q odd or ≡ 2 mod 4 (the workspace sub-buffers must stay aligned for the
+    prologue's 8-B and the segment kernel's 16-B stores): every entry point against the oracle."""
+    torch = _torch()
+    rng = np.random.default_rng(1000 * B + 10 * Hq + Hkv)
+    fmt = O.PageFormat(128, 2, 64, 64)
+    L = [int(x) for x in rng.integers(1, 200, B)]
+    pt, pool, RK, RV = _oracle_pool(rng, fmt, B, Hkv, L)
+    q = synth.gen_decode_q(rng, B, Hq, 128)
+    o = make(num_q_heads=Hq, num_kv_heads=Hkv, bits=2, group_size=64)
+    mp = pt.shape[1]
+    ws = torch.empty(o.attend_workspace_bytes(B, mp), dtype=torch.uint8, device="cuda")
+    out = torch.empty((B, Hq, 128), dtype=torch.float32, device="cuda")
+    if call == "attend":
+        o.attend(T(q, torch.bfloat16), T(pt), T(np.asarray(L, np.int32)), T(pool), T(RK), T(RV), ws, out)
+        ref, _ = O.attend(q, pt, L, pool, RK, RV, fmt, Hkv)
+    elif call == "decode_step":
+        kn, vn = synth.gen_keys(rng, B, Hkv, 128), synth.gen_values(rng, B, Hkv, 128)
+        L1 = [x + 1 for x in L]
+        mp1 = (max(L1) + 63) // 64
+        if mp1 > mp:                                 # room for the new row
+            pt = np.concatenate([pt, np.arange(pool.shape[0], pool.shape[0] + B, dtype=np.int32)[:, None]], 1)
+            pool = np.concatenate([pool, np.zeros((B, Hkv, fmt.page_bytes), np.uint8)])
+            ws = torch.empty(o.attend_workspace_bytes(B, pt.shape[1]), dtype=torch.uint8, device="cuda")
+        ref_pool = pool.copy()
+        ns = np.array([pt[b, (L1[b] - 1) // 64] * 64 + (L1[b] - 1) % 64 for b in range(B)], np.int64)
+        O.quantize_append(kn, vn, ns, RK, RV, fmt, ref_pool)
+        ref, _ = O.attend(q, pt, L1, ref_pool, RK, RV, fmt, Hkv)
+        gp = T(pool)
+        o.decode_step(T(q, torch.bfloat16), T(kn, torch.bfloat16), T(vn, torch.bfloat16), T(pt),
+                      T(np.asarray(L1, np.int32)), gp, T(RK), T(RV), ws, out)
+    else:
+        cap = 8
+        sk = synth.gen_keys(rng, B * Hkv * cap, 1, 128).reshape(B, Hkv, cap, 128)
+        sv = synth.gen_values(rng, B * Hkv * cap, 1, 128).reshape(B, Hkv, cap, 128)
+        sl = rng.integers(0, cap + 1, B).astype(np.int32)
+        o.attend_mixed(T(q, torch.bfloat16), T(pt), T(np.asarray(L, np.int32)), T(pool), T(RK), T(RV),
+                       T(sk, torch.bfloat16), T(sv, torch.bfloat16), T(sl), ws, out)
+        ref, _ = O.attend_mixed(q, pt, L, pool, sk, sv, sl, RK, RV, fmt, Hkv)
+    torch.cuda.synchronize()
+    assert np.abs(out.cpu().numpy() - ref).max() <= 2e-3
 
 
 def test_attend_page_indirection_invariance():

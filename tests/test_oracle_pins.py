@@ -87,6 +87,97 @@ def test_compose_pbr_convention_pinned_exactly():
     assert sorted(WE["K_UQ_H"].tolist()) == sorted(WE["K_UQ_H_P"].tolist())
 
 
+def test_rotate_pinned_by_printed_rows():
+    """App A.5 P:L1229-1233 x̃ = x·R, row-vector convention, checked through O.rotate
+    itself on the printed worked example: raw K_t · H = the printed pure-Hadamard row
+    (P:L163 -> P:L255); K U_Q · H = P:L209-217; K U_Q · (H P_br) = the printed OSCAR row
+    (P:L186 -> P:L232).  Two heads with different R pin the per-head indexing; the transposed
+    operand (x · Rᵀ, what a swapped einsum would compute) is excluded by a cyclic-shift R."""
+    H = O.hadamard(128)
+    R0 = O.compose_rotation(np.eye(128))
+    X = np.stack([WE["raw_K_t"], WE["K_UQ"], WE["K_UQ"]])[None]          # [T=1, heads=3, d]
+    R = np.stack([H, H, R0]).astype(np.float32)
+    out = O.rotate(X, R)
+    assert out.dtype == np.float32 and out.shape == (1, 3, 128)
+    assert np.abs(out[0, 0] - WE["K_H"]).max() < 0.02
+    assert np.abs(out[0, 1] - WE["K_UQ_H"]).max() < 0.02
+    assert np.abs(out[0, 2] - WE["K_UQ_H_P"]).max() < 0.02
+    # H P_br is symmetric (P_br H P_br = H for Sylvester H), so the orientation x·R vs x·Rᵀ is
+    # pinned by a non-symmetric closed form: R[k][(k+1) mod d] = 1 gives (x R)_j = x_{j-1}
+    Sh = np.roll(np.eye(128, dtype=np.float32), 1, axis=1)
+    sh = O.rotate(X[:, :1], Sh[None])
+    assert np.array_equal(sh[0, 0], np.roll(WE["raw_K_t"], 1).astype(np.float32))
+    # rows are independent (token axis): a second token equal to the first gives the same row
+    out2 = O.rotate(np.concatenate([X, X * 2]), R)
+    assert np.array_equal(out2[0], out[0]) and np.allclose(out2[1], 2 * out[0], rtol=1e-6, atol=1e-6)
+
+
+def _beta(j, m):
+    return int(format(j, f"0{m}b")[::-1], 2)
+
+
+def test_calibrate_from_sums_closed_forms():
+    """Alg. 1 Calibrate: C = acc / n_rows, EigVec descending, R = U H P_br
+    (Eq. 3), R_K from the C_Q sums and R_V from the C_S sums.  Diagonal sums have
+    U = a permutation known in closed form, so R and λ are written out independently with
+    scipy's Sylvester Hadamard and a string bit reversal."""
+    from scipy.linalg import hadamard as sylvester
+    d, n = 128, 37
+    Hs = sylvester(d) / math.sqrt(d)
+    lam = np.linspace(9.0, 0.5, d)                     # distinct, descending
+    acc_q = np.diag(lam * n)[None]                     # C_Q = diag(λ): U = I
+    acc_s = np.diag(lam[::-1] * n)[None]               # C_S = diag(λ ascending): U = J (reversal)
+    R_K, R_V, lam_q, lam_s = O.calibrate_from_sums(acc_q, acc_s, n)
+    Rk_exp = np.empty((d, d))
+    Rv_exp = np.empty((d, d))
+    for j in range(d):
+        Rk_exp[:, j] = Hs[:, _beta(j, 7)]              # (x U H P_br)_j = (x U H)_{β(j)}
+        Rv_exp[:, j] = Hs[::-1, _beta(j, 7)]           # U = J reverses the rows of H
+    assert np.abs(R_K[0] - Rk_exp).max() < 1e-7 and np.abs(R_V[0] - Rv_exp).max() < 1e-7
+    np.testing.assert_allclose(lam_q[0], lam, rtol=1e-12)          # λ of acc / n_rows, descending
+    np.testing.assert_allclose(lam_s[0], lam, rtol=1e-12)
+    # a 4 x 4 case with a non-trivial eigenvector pair: [[3,1],[1,3]] ⊕ diag(1, 0.5)
+    C4 = np.array([[3, 1, 0, 0], [1, 3, 0, 0], [0, 0, 1, 0], [0, 0, 0, 0.5]], float)
+    R4, _, l4, _ = O.calibrate_from_sums((C4 * 5)[None], np.eye(4)[None], 5)
+    s = 1 / math.sqrt(2)
+    U = np.array([[s, s, 0, 0], [s, -s, 0, 0], [0, 0, 1, 0], [0, 0, 0, 1]])   # sign rule: ties -> first +
+    UH = U @ (sylvester(4) / 2)
+    exp = np.stack([UH[:, _beta(j, 2)] for j in range(4)], axis=1)
+    np.testing.assert_allclose(l4[0], [4, 2, 1, 0.5], rtol=1e-12)
+    assert np.abs(R4[0] - exp).max() < 1e-7
+
+
+def test_quantizer_codes_are_the_real_arithmetic_round():
+    """Reading Z4 pinned to App A.5's real arithmetic: with the stored (s16, m16),
+    Q+ = clip(round((x - m16)/s16), 0, q_max) in exact rational arithmetic (Python fractions).
+    The oracle's two fp32 roundings (RN(x - m16), RN(1/s16)) may only move t by |t|·2^-22, so
+    codes agree except within that distance of a .5 boundary — and such cases are rare."""
+    from fractions import Fraction
+    rng = np.random.default_rng(44)
+    for bits, G in [(2, 64), (3, 32), (4, 128)]:
+        qmax = 2 ** bits - 1
+        X = (rng.standard_normal((40, 128)) * rng.uniform(0.01, 20, (40, 1))).astype(np.float32)
+        codes, s16, m16 = O.quantize_rows(X, bits, G)
+        n_near = 0
+        for r in range(X.shape[0]):
+            for c in range(128):
+                gi = c // G
+                s = Fraction(float(s16[r, gi]))
+                if s == 0:
+                    assert codes[r, c] == 0
+                    continue
+                t = (Fraction(float(X[r, c])) - Fraction(float(m16[r, gi]))) / s
+                k = math.floor(t + Fraction(1, 2))
+                if t + Fraction(1, 2) == k and k % 2 == 1:   # exact tie -> even
+                    k -= 1
+                exp = min(max(k, 0), qmax)
+                if codes[r, c] != exp:
+                    frac = t - math.floor(t)
+                    assert abs(float(frac) - 0.5) <= abs(float(t)) * 2.0 ** -22 + 1e-12, (bits, G, r, c)
+                    n_near += 1
+        assert n_near <= 2
+
+
 def test_group_range_statistic_printed():
     for row, key in [("raw_K_t", "group_range_raw"), ("K_UQ", "group_range_UQ"),
                      ("K_UQ_H", "group_range_UQH"), ("K_UQ_H_P", "group_range_UQHP"),

@@ -3,14 +3,15 @@
 NVCC ?= nvcc
 PKG := paper_2605_17757_b200
 SRC := $(wildcard $(PKG)/csrc/*.cu)
-OBJDIR := build/obj
+OBJDIR ?= build/obj
+LIB ?= $(PKG)/liboscar.so
 OBJ := $(patsubst $(PKG)/csrc/%.cu,$(OBJDIR)/%.o,$(SRC))
 HDR := $(wildcard $(PKG)/csrc/*.cuh) include/oscar.h
 NVFLAGS := -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 \
            -Xcompiler -fPIC -Xcompiler -fvisibility=hidden -Iinclude -I$(PKG)/csrc \
            --expt-relaxed-constexpr -Xptxas -warn-spills $(EXTRA_NVFLAGS)
 
-$(PKG)/liboscar.so: $(OBJ)
+$(LIB): $(OBJ)
 	$(NVCC) -gencode arch=compute_100a,code=sm_100a -shared -o $@ $(OBJ) -lcudart
 
 $(OBJDIR)/%.o: $(PKG)/csrc/%.cu $(HDR)
@@ -18,6 +19,6 @@ $(OBJDIR)/%.o: $(PKG)/csrc/%.cu $(HDR)
 	$(NVCC) $(NVFLAGS) -c -o $@ $<
 
 clean:
-	rm -rf $(PKG)/liboscar.so $(OBJDIR)
+	rm -rf $(LIB) $(OBJDIR)
 
 .PHONY: clean

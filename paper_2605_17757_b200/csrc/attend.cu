@@ -83,6 +83,9 @@ __global__ void __launch_bounds__(512) attend_prologue_kernel(PrologueParams pp)
     }
   }
   if (pp.work && b == 0 && h == 0 && tid == 0) *pp.work = 0;   // reset the work-item counter
+#ifdef OSCAR_PROBE_NOPRO
+  return;                                            // timing probe only (results invalid)
+#endif
   // this warp's 8 rows of R_K (and R_V) are loaded first: their latency overlaps the row loads
   const bool rv = dec && pp.RV;
   float4 rk[8], rvv[8];
@@ -433,6 +436,9 @@ __global__ void __launch_bounds__(256) attend_merge_kernel(AttnParams p, const f
   __shared__ __align__(16) float ot[HC][kD];
   __shared__ float pm[8], pl[8], sws[HC];
   __shared__ __align__(8) uint64_t bar;
+#ifdef OSCAR_PROBE_NOMERGE
+  return;                                            // timing probe only (results invalid)
+#endif
   const int b = blockIdx.x, h = blockIdx.y, tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   const int hz = blockIdx.z * HC;                    // first query head (within the group) of this CTA
   if (RV && tid == 0) {

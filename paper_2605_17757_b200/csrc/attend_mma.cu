@@ -184,6 +184,10 @@ attend_partial_mma(AttnParams p, int S) {
   constexpr uint32_t kByteMask = BITS == 2 ? 0x03030303u : 0x0F0F0F0Fu;
   extern __shared__ __align__(128) unsigned char smem[];
 
+#ifdef OSCAR_PROBE_NOPARTIAL
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  return;                                            // timing probe only (results invalid)
+#endif
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gid = lane >> 2, t = lane & 3;
   const int page_bytes = p.page_bytes, P = p.P;

@@ -113,9 +113,9 @@ def _slots(rng, mode, Tn, npages):
     if mode == "perm":
         return rng.permutation(npages * 64)[:Tn].astype(np.int64)
     start = int(mode[6:])
-    run = np.arange(start, start + 700)
+    run = np.arange(start, start + min(700, Tn))
     rest = np.setdiff1d(np.arange(npages * 64), run)
-    return np.concatenate([run, rng.permutation(rest)[:Tn - 700]]).astype(np.int64)
+    return np.concatenate([run, rng.permutation(rest)[:Tn - len(run)]]).astype(np.int64)
 
 
 def check_append_flips(got, K, V, RK, RV, slots, fmt, rho=(1.0, 1.0)):

@@ -1,9 +1,9 @@
 #!/bin/bash
-# Build an A/B variant of liboscar.so with extra nvcc defines: tools/build_variant.sh NAME -DFOO=1 ...
+# Build an A/B variant of liboscar.so with extra nvcc defines (parallel, objects under build/):
+#   tools/build_variant.sh NAME -DFOO=1 ...   ->  build_ab/liboscar_NAME.so
 set -e
 cd "$(dirname "$0")/.."
 name=$1; shift
 mkdir -p build_ab
-nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC \
-  -Xcompiler -fvisibility=hidden -Iinclude -Ipaper_2605_17757_b200/csrc --expt-relaxed-constexpr \
-  "$@" -shared -o build_ab/liboscar_$name.so paper_2605_17757_b200/csrc/*.cu -lcudart
+make -s -j8 OBJDIR=build/v_$name LIB=build_ab/liboscar_$name.so EXTRA_NVFLAGS="$*" 2>&1 | grep -v spill || true
+ls -la build_ab/liboscar_$name.so

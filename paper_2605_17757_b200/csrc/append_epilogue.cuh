@@ -62,9 +62,10 @@ __device__ __forceinline__ float warp_row_rank_select(const float a[4], int k) {
 }
 
 // One warp owns one row: lane holds channels 4*lane .. 4*lane+3 in y[] (bits in {2, 3, 4}).
+// deq (optional): the lane's 4 dequantized values s16·c + m16 (App A.5), fp32
 __device__ __forceinline__ void quantize_store_row_warp(const EpiParams& ep, float y[4], int lane,
                                                         int64_t slot, int h, int isV,
-                                                        uint8_t* __restrict__ pool) {
+                                                        uint8_t* __restrict__ pool, float* deq = nullptr) {
   const int cidx = isV ? ep.clip_v_idx : ep.clip_k_idx;
   if (cidx >= 0) {
     const float a[4] = {fabsf(y[0]), fabsf(y[1]), fabsf(y[2]), fabsf(y[3])};
@@ -86,7 +87,13 @@ __device__ __forceinline__ void quantize_store_row_warp(const EpiParams& ep, flo
   int c[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) c[i] = quant_code(y[i], m, inv, qmax);
+  if (deq) {
+    const float sf = __half2float(s16);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) deq[i] = fmaf(sf, (float)c[i], m);
+  }
 
+  if (!pool) return;                          // (dequantized values only)
   const int64_t page = slot / ep.P;
   const int off = (int)(slot % ep.P);
   uint8_t* blk = pool + (page * ep.hkv + h) * (int64_t)ep.page_bytes;

@@ -18,27 +18,24 @@
 namespace oscar {
 
 // ------------------------------------------------------------------ prologue
-// q rotation (B1), and in decode-step mode also the step's quantize-append (Alg. 1 DecodeStep
-// appends the new row before attending; QuantizeAndWrite P:L1639-1643).
-// grid (B, H_kv), 512 threads (16 warps).  Rows rotated per CTA: the GQ query heads of group h
-// and the new K row by R_K[h], the new V row by R_V[h].  Warp w owns the contraction slice
-// k = 8w .. 8w+7: it loads those 8 rows of R_K (and R_V) once — lane l the float4 of columns
-// 4l..4l+3, 16 loads in flight — and forms partial dots for every row vector; the 16 partials
-// per (row, channel) are summed through smem.  Then:
-//   * warps 0..GQ-1: q̃ = q·R_K·scale·log₂e (fp32, kept for the simple kernel) and the 15-bit
-//     integer form of the IMMA QK path: qscale = max|q̃| / 32639, qint = rint(q̃/qscale)
-//     (|qint| <= 32639 = 127·256 + 127, so the hi/lo int8 split never overflows), qsum[grp] =
-//     Σ_{c in grp} qint; then all threads write the per-lane IMMA A fragments of the group;
-//   * decode step: warp 14 quantizes and stores the K row, warp 15 the V row, at position
-//     seq_lens[b] - 1 of sequence b (the shared clip/min-max/pack epilogue of quantize_append).
+// q rotation (B1): grid (B, H_kv), 512 threads (16 warps).  Rows rotated per CTA: the GQ query
+// heads of group h by R_K[h].  Warp w owns the contraction slice k = 8w .. 8w+7: it loads those
+// 8 rows of R_K once — lane l the float4 of columns 4l..4l+3, 8 loads in flight — and forms
+// partial dots for every query row; the 16 partials per (row, channel) are summed through smem.
+// Then:
+//   * warps 0..GQ-1: q̃ = q·R_K·scale·log₂e (fp32, kept for the simple kernel and for the decode
+//     step's new-token logit) and the 15-bit integer form of the IMMA QK path: qscale = max|q̃| /
+//     32639, qint = rint(q̃/qscale) (|qint| <= 32639 = 127·256 + 127, so the hi/lo int8 split
+//     never overflows), qsum[grp] = Σ_{c in grp} qint; then all threads write the per-lane IMMA
+//     operand fragments of the group.
+// (The decode step's QuantizeAndWrite of the new K/V row runs in the merge kernel, off the
+// partial kernel's critical path — see attend_merge_kernel.)
 // PDL: launched as an ordinary kernel (every earlier kernel of the stream is complete when it
-// starts) and lets the partial kernel launch at once; the partial kernel's page prefetch only
-// touches pages this kernel does not write (the last page of each sequence waits for
-// griddepcontrol.wait).
+// starts) and lets the partial kernel launch at once; the partial kernel's early page prefetch
+// only reads pool pages, which nothing in this call writes before the merge kernel.
 struct PrologueParams {
   const uint16_t* q;            // [B][H_q][128] bf16
   const float* RK;              // [H_kv][128][128]
-  const float* RV;              // [H_kv][128][128] or null (pre-rotated V)
   int Hq, lgG, bits, nt;
   float qscale;                 // softmax scale · log2(e)
   float* qt;
@@ -48,96 +45,60 @@ struct PrologueParams {
   uint32_t* qfrag;              // null: simple kernel path
   int tq;                       // 1: fragments for the token-row QK layout of attend_partial_mma
   int32_t* work;                // null: simple kernel path
-  // decode step (null knew: plain attend)
-  const uint16_t* knew;         // [B][H_kv][128] bf16
-  const uint16_t* vnew;
-  const int32_t* page_table;
-  const int32_t* seq_lens;
-  int max_pages;
-  uint8_t* pool;
-  EpiParams ep;
 };
 
 template <int GQ>
 __global__ void __launch_bounds__(512) attend_prologue_kernel(PrologueParams pp) {
-  constexpr int NR = GQ + 2;                         // q heads, K row, V row
+  constexpr int NR = GQ;                             // q heads
   extern __shared__ __align__(16) float psm[];
   float* ps = psm;                                   // [16][NR][128] partial dots
   __shared__ __align__(16) float xs[NR][kD];         // input rows (fp32)
   __shared__ __align__(16) float ys[NR][kD];         // rotated rows
   __shared__ int16_t qis[GQ][kD];
+  // launched with PDL behind whatever precedes it on the stream: wait for it first (q, R_K and
+  // the pool may be its outputs), then let the partial kernel launch
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   const int b = blockIdx.x, h = blockIdx.y, tid = threadIdx.x;
   const int w = tid >> 5, lane = tid & 31;
   const int G = 1 << pp.lgG;
-  const bool dec = pp.knew != nullptr;
-  // decode step: the new row's slot (two dependent global loads) is fetched first, so its
-  // latency hides behind the R loads instead of sitting on the append's critical path
-  int slot_L = 0;
-  int64_t slot_new = 0;
-  if (dec && w >= 14) {
-    slot_L = pp.seq_lens[b];
-    if (slot_L > 0) {
-      const int pos = slot_L - 1;
-      slot_new = (int64_t)pp.page_table[(size_t)b * pp.max_pages + pos / pp.ep.P] * pp.ep.P + pos % pp.ep.P;
-    }
-  }
   if (pp.work && b == 0 && h == 0 && tid == 0) *pp.work = 0;   // reset the work-item counter
 #ifdef OSCAR_PROBE_NOPRO
   return;                                            // timing probe only (results invalid)
 #endif
-  // this warp's 8 rows of R_K (and R_V) are loaded first: their latency overlaps the row loads
-  const bool rv = dec && pp.RV;
-  float4 rk[8], rvv[8];
+  // this warp's 8 rows of R_K are loaded first: their latency overlaps the row loads
+  float4 rk[8];
   {
     const float4* RK4 = reinterpret_cast<const float4*>(pp.RK + (size_t)h * kD * kD) + (size_t)8 * w * 32 + lane;
 #pragma unroll
     for (int i = 0; i < 8; ++i) rk[i] = __ldg(RK4 + i * 32);
-    if (rv) {
-      const float4* RV4 = reinterpret_cast<const float4*>(pp.RV + (size_t)h * kD * kD) + (size_t)8 * w * 32 + lane;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) rvv[i] = __ldg(RV4 + i * 32);
-    }
   }
   for (int e = tid; e < NR * (kD / 4); e += 512) {
     const int r = e >> 5, l4 = e & 31;
-    const uint16_t* src = r < GQ ? pp.q + ((size_t)b * pp.Hq + (size_t)h * GQ + r) * kD
-                        : (dec ? (r == GQ ? pp.knew : pp.vnew) + ((size_t)b * gridDim.y + h) * kD : nullptr);
-    float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (src) {
-      const uint2 u = reinterpret_cast<const uint2*>(src)[l4];
-      f = make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xffff0000u),
-                      __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xffff0000u));
-    }
-    reinterpret_cast<float4*>(xs[r])[l4] = f;
+    const uint16_t* src = pp.q + ((size_t)b * pp.Hq + (size_t)h * GQ + r) * kD;
+    const uint2 u = reinterpret_cast<const uint2*>(src)[l4];
+    reinterpret_cast<float4*>(xs[r])[l4] =
+        make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xffff0000u),
+                    __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xffff0000u));
   }
   __syncthreads();
-  {
 #pragma unroll
-    for (int r = 0; r < NR; ++r) {
-      if (r > GQ && !rv) break;
-      if (r == GQ && !dec) break;
-      float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int r = 0; r < NR; ++r) {
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float x = xs[r][8 * w + i];
-        const float4 m = r <= GQ ? rk[i] : rvv[i];
-        a.x = fmaf(x, m.x, a.x); a.y = fmaf(x, m.y, a.y); a.z = fmaf(x, m.z, a.z); a.w = fmaf(x, m.w, a.w);
-      }
-      reinterpret_cast<float4*>(ps + ((size_t)w * NR + r) * kD)[lane] = a;
+    for (int i = 0; i < 8; ++i) {
+      const float x = xs[r][8 * w + i];
+      const float4 m = rk[i];
+      a.x = fmaf(x, m.x, a.x); a.y = fmaf(x, m.y, a.y); a.z = fmaf(x, m.z, a.z); a.w = fmaf(x, m.w, a.w);
     }
+    reinterpret_cast<float4*>(ps + ((size_t)w * NR + r) * kD)[lane] = a;
   }
   __syncthreads();
   for (int e = tid; e < NR * kD; e += 512) {
     const int r = e >> 7, c = e & (kD - 1);
-    float y;
-    if (r == GQ + 1 && !pp.RV) {
-      y = xs[r][c];                                  // pre-rotated V (NEXT-2): identity
-    } else {
-      y = 0.f;
+    float y = 0.f;
 #pragma unroll
-      for (int ww = 0; ww < 16; ++ww) y += ps[((size_t)ww * NR + r) * kD + c];
-    }
+    for (int ww = 0; ww < 16; ++ww) y += ps[((size_t)ww * NR + r) * kD + c];
     ys[r][c] = y;
   }
   __syncthreads();
@@ -162,13 +123,6 @@ __global__ void __launch_bounds__(512) attend_prologue_kernel(PrologueParams pp)
     int gs = v0 + v1 + v2 + v3;                    // lanes of one group: G/4 consecutive lanes
     for (int o = 1; o < (G >> 2); o <<= 1) gs += __shfl_xor_sync(0xffffffffu, gs, o);
     if ((lane & ((G >> 2) - 1)) == 0) pp.qsum[row * 8 + (lane * 4 >> pp.lgG)] = gs;
-  } else if (dec && w >= 14) {
-    const int isV = w - 14;
-    if (slot_L > 0) {
-      const float4 y4 = reinterpret_cast<const float4*>(ys[GQ + isV])[lane];
-      float y[4] = {y4.x, y4.y, y4.z, y4.w};
-      quantize_store_row_warp(pp.ep, y, lane, slot_new, h, isV, pp.pool);
-    }
   }
   __syncthreads();
   // IMMA A fragments for attend_partial_mma: word (j, kk, r) of lane (gid, t) holds the
@@ -249,7 +203,7 @@ __global__ void __launch_bounds__(128) attend_partial_simple(AttnParams p) {
   const int split = blockIdx.x, h = blockIdx.y, b = blockIdx.z, tid = threadIdx.x;
   constexpr int g = GQ;
   const int P = p.P;
-  const int seq_len = p.seq_lens[b];
+  const int seq_len = max(p.seq_lens[b] - p.len_adj, 0);
   const int page0 = split * p.pps;
   const int page1 = min(page0 + p.pps, (seq_len + P - 1) / P);
 
@@ -412,35 +366,59 @@ __global__ void __launch_bounds__(128) attend_partial_simple(AttnParams p) {
 // grid (B, H_kv, g / HC), 256 threads (8 warps): one CTA per (sequence, KV head) and HC query
 // heads of its group — HC = g normally (the heads share one copy of R_V[h]), HC = 1 for small
 // batches (more CTAs, more warps per head's splits).  Before griddepcontrol.wait (it only touches the
-// caller's inputs) R_V[h] (64 KB) is bulk-copied into smem.  Then warp w serves head w mod g,
+// caller's inputs and the prologue's q̃) R_V[h] (64 KB) is bulk-copied into smem.  Then warp w serves head w mod g,
 // splits s ≡ w / g (mod 8/g): each lane issues all loads of a batch of up to 16 splits at once
 // (partial row float4 = channels 4l..4l+3, split max and sum) and folds them with a running max;
 // the 8/g warps of a head and the NEXT-1 segment are combined through smem.  Un-rotation:
 // thread (c', half) forms output channel c' of every other head from smem, the contraction index
 // rotated by lane (c = 4·((k + lane) mod 32)) so the 32 rows of a warp hit distinct banks.
+//
+// Decode step (Alg. 1 DecodeStep; reading Z35): the partial kernel attends over the
+// first seq_len - 1 tokens of the pool; this kernel, BEFORE griddepcontrol.wait (so the work
+// overlaps the partial kernel's tail), runs QuantizeAndWrite of the step's new K/V
+// row — x̃ = x·R (warp w contracts rows 16w..16w+15 of R_K from L2 / R_V from smem), the shared
+// clip/min-max/pack epilogue, store at slot page_table[b][(L-1)/P]·P + (L-1)%P (one CTA per
+// (b, h) stores) — and folds the new token as one more partial: logit q̃·k̂ of its DEQUANTIZED
+// key (k̂ = s16·c + m16, exactly what the pool now holds), weight 1, value v̂.  Same result as
+// appending first and attending over seq_len tokens.
 namespace {
 __device__ __forceinline__ uint32_t msmem_u32(const void* ptr) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(ptr));
 }
 }  // namespace
 
+struct StepParams {
+  const uint16_t* knew;         // [B][H_kv][128] bf16; null: plain attend
+  const uint16_t* vnew;
+  const float* RK;              // [H_kv][128][128]
+  const int32_t* page_table;
+  const int32_t* seq_lens;
+  int max_pages;
+  uint8_t* pool;
+  EpiParams ep;
+};
+
 template <int HC>
 __global__ void __launch_bounds__(256) attend_merge_kernel(AttnParams p, const float* __restrict__ RV,
                                                            void* __restrict__ out, int out_fp32,
-                                                           float* __restrict__ lse) {
+                                                           float* __restrict__ lse, StepParams sp) {
+#ifdef OSCAR_PROBE_NOMERGE
+  return;                                            // timing probe only (results invalid)
+#endif
   constexpr int WPH = 8 / HC;                        // warps per query head
   constexpr int NB = 8;                              // splits per load batch (two in flight) per warp
   constexpr int HPT = (HC + 1) / 2;                  // heads per thread in the un-rotation
   extern __shared__ __align__(128) float Rs[];       // [128][128] R_V[h]
   __shared__ __align__(16) float po[8][kD];
   __shared__ __align__(16) float ot[HC][kD];
-  __shared__ float pm[8], pl[8], sws[HC];
+  __shared__ __align__(16) float nrow[2][kD];        // decode step: new K / V row, then k̂ / v̂
+  __shared__ float pm[8], pl[8], sws[HC], nlog[HC];
   __shared__ __align__(8) uint64_t bar;
-#ifdef OSCAR_PROBE_NOMERGE
-  return;                                            // timing probe only (results invalid)
-#endif
   const int b = blockIdx.x, h = blockIdx.y, tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   const int hz = blockIdx.z * HC;                    // first query head (within the group) of this CTA
+  // the next call's prologue may become resident now: it waits for this grid's completion
+  // before touching anything
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   if (RV && tid == 0) {
     const uint32_t bb = msmem_u32(&bar);
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bb));
@@ -451,12 +429,124 @@ __global__ void __launch_bounds__(256) attend_merge_kernel(AttnParams p, const f
                  "l"(RV + (size_t)h * kD * kD), "r"(kD * kD * 4), "r"(bb)
                  : "memory");
   }
+  auto wait_rv = [&]() {
+    asm volatile(
+        "{\n.reg .pred P1;\nWAIT_R%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n"
+        "@!P1 bra WAIT_R%=;\n}\n" ::"r"(msmem_u32(&bar))
+        : "memory");
+  };
+  // ---- decode step: QuantizeAndWrite of the new row + its attention partial (pre-wait)
+  const int Lnew = sp.knew ? sp.seq_lens[b] : 0;
+  if (Lnew > 0) {
+    __syncthreads();                                 // bar initialised before anyone waits on it
+    if (w < 2) {
+      const uint16_t* src = (w ? sp.vnew : sp.knew) + ((size_t)b * p.hkv + h) * kD;
+      const uint2 u = reinterpret_cast<const uint2*>(src)[lane];
+      reinterpret_cast<float4*>(nrow[w])[lane] =
+          make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xffff0000u),
+                      __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xffff0000u));
+    }
+    __syncthreads();
+    // x̃ partial dots: warp w contracts rows 16w..16w+15 (lane: columns 4l..4l+3); K with R_K
+    // from L2 (16 float4 in flight), V with R_V from smem (identity when R_V = NULL)
+    {
+      const float4* RK4 = reinterpret_cast<const float4*>(sp.RK + (size_t)h * kD * kD) + (size_t)16 * w * 32 + lane;
+      float4 rk[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) rk[i] = __ldg(RK4 + i * 32);
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float x = nrow[0][16 * w + i];
+        a.x = fmaf(x, rk[i].x, a.x); a.y = fmaf(x, rk[i].y, a.y); a.z = fmaf(x, rk[i].z, a.z); a.w = fmaf(x, rk[i].w, a.w);
+      }
+      reinterpret_cast<float4*>(po[w])[lane] = a;
+    }
+    float4 av = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (RV) {
+      wait_rv();
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float x = nrow[1][16 * w + i];
+        const float4 r = reinterpret_cast<const float4*>(Rs + (size_t)(16 * w + i) * kD)[lane];
+        av.x = fmaf(x, r.x, av.x); av.y = fmaf(x, r.y, av.y); av.z = fmaf(x, r.z, av.z); av.w = fmaf(x, r.w, av.w);
+      }
+    }
+    __syncthreads();
+    float y = 0.f;                                   // thread c (< 128): x̃_K[c]; 128 + c: x̃_V[c]
+    {
+      const int c = tid & (kD - 1);
+      if (tid < kD) {
+#pragma unroll
+        for (int ww = 0; ww < 8; ++ww) y += po[ww][c];
+      }
+    }
+    __syncthreads();
+    reinterpret_cast<float4*>(po[w])[lane] = av;     // V partials reuse po
+    __syncthreads();
+    if (tid >= kD) {
+      const int c = tid - kD;
+      if (RV) {
+#pragma unroll
+        for (int ww = 0; ww < 8; ++ww) y += po[ww][c];
+      } else {
+        y = nrow[1][c];                              // pre-rotated V (NEXT-2): identity
+      }
+    }
+    __syncthreads();
+    nrow[tid >> 7][tid & (kD - 1)] = y;
+    __syncthreads();
+    if (w < 2) {                                     // warp 0: K row, warp 1: V row
+      const int pos = Lnew - 1;
+      const int64_t slot = (int64_t)sp.page_table[(size_t)b * sp.max_pages + pos / sp.ep.P] * sp.ep.P + pos % sp.ep.P;
+      const float4 y4 = reinterpret_cast<const float4*>(nrow[w])[lane];
+      float yy[4] = {y4.x, y4.y, y4.z, y4.w}, dq[4];
+      quantize_store_row_warp(sp.ep, yy, lane, slot, h, w, blockIdx.z == 0 ? sp.pool : nullptr, dq);
+      __syncwarp();
+      reinterpret_cast<float4*>(nrow[w])[lane] = make_float4(dq[0], dq[1], dq[2], dq[3]);
+    }
+    __syncthreads();
+    if (w < HC) {                                    // new-token logit (log2 units): q̃·k̂
+      const size_t row = (size_t)b * p.hq + (size_t)h * p.g + hz + w;
+      const float4 qv = __ldcg(reinterpret_cast<const float4*>(p.qt + row * kD) + lane);
+      const float4 kv = reinterpret_cast<const float4*>(nrow[0])[lane];
+      float d = qv.x * kv.x + qv.y * kv.y + qv.z * kv.z + qv.w * kv.w;
+      for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+      if (lane == 0) nlog[w] = d;
+    }
+  }
+  // split partials of this unit: all n_splits slots (simple kernel), or the count of warps whose
+  // range covers the unit under the balanced decomposition (attend_mma.cu, Decomp)
+  int ns = p.n_splits;
+  if (p.balanced) {
+    __shared__ int red[2][8];
+    int lt = 0, tot = 0;
+    for (int bb = tid; bb < p.batch; bb += 256) {
+      const int n = (max(p.seq_lens[bb] - p.len_adj, 0) + p.P - 1) / p.P;
+      tot += n;
+      lt += bb < b ? n : 0;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      lt += __shfl_xor_sync(0xffffffffu, lt, o);
+      tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    }
+    if (lane == 0) { red[0][w] = lt; red[1][w] = tot; }
+    __syncthreads();
+    lt = 0; tot = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { lt += red[0][i]; tot += red[1][i]; }
+    const int npg = (max(p.seq_lens[b] - p.len_adj, 0) + p.P - 1) / p.P;
+    const int64_t T = tot;
+    const int64_t W = min((int64_t)(p.n_warps / p.hkv), max((int64_t)1, T / p.pmin));
+    auto rof = [&](int64_t x) { return ((x + 1) * W - 1) / T; };
+    ns = npg > 0 ? (int)(rof(lt + npg - 1) - rof(lt) + 1) : 0;
+  }
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
-  const int ns = p.n_splits;
   {
     const int hd = w % HC, part = w / HC;
     const size_t rbh = (size_t)b * p.hq + (size_t)h * p.g + hz + hd;
-    auto prow = [&](int s) -> size_t { return rbh * ns + s; };
+    auto prow = [&](int s) -> size_t { return rbh * p.n_splits + s; };
     float mw = -INFINITY, Lw = 0.f;
     float4 ow = make_float4(0.f, 0.f, 0.f, 0.f);
     // software-pipelined fold: the loads of the next batch of NB splits are in flight while
@@ -500,6 +590,7 @@ __global__ void __launch_bounds__(256) attend_merge_kernel(AttnParams p, const f
       if (s0 + 2 * STEP < ns) load(s0 + 2 * STEP, xa, ma, la);
       fold(xb, mb, lb);
     }
+    __syncthreads();                                 // (decode step) po was scratch above
     reinterpret_cast<float4*>(po[w])[lane] = ow;
     if (lane == 0) { pm[w] = mw; pl[w] = Lw; }
   }
@@ -508,7 +599,8 @@ __global__ void __launch_bounds__(256) attend_merge_kernel(AttnParams p, const f
   for (int e = tid; e < HC * kD; e += 256) {
     const int hd = e >> 7, c = e & (kD - 1);
     const size_t row = (size_t)b * p.hq + (size_t)h * p.g + hz + hd;
-    float M = seg ? p.seg_m[row] : -INFINITY;
+    const float mnew = Lnew > 0 ? nlog[hd] : -INFINITY;
+    float M = fmaxf(seg ? p.seg_m[row] : -INFINITY, mnew);
 #pragma unroll
     for (int j = 0; j < WPH; ++j) M = fmaxf(M, pm[hd + HC * j]);
     float L = 0.f, o = 0.f;
@@ -518,6 +610,11 @@ __global__ void __launch_bounds__(256) attend_merge_kernel(AttnParams p, const f
         const float wj = exp2f(pm[hd + HC * j] - M);
         L = fmaf(pl[hd + HC * j], wj, L);
         o = fmaf(po[hd + HC * j][c], wj, o);
+      }
+      if (Lnew > 0) {                                // the step's new token: weight 1, value v̂
+        const float wn = exp2f(mnew - M);
+        L += wn;
+        o = fmaf(nrow[1][c], wn, o);
       }
     }
     const float wseg = (seg && M != -INFINITY) ? exp2f(p.seg_m[row] - M) : 0.f;
@@ -533,11 +630,7 @@ __global__ void __launch_bounds__(256) attend_merge_kernel(AttnParams p, const f
   const int cp = tid & (kD - 1), hh = tid >> 7;
   float acc[HPT];
   if (RV) {
-    asm volatile(
-        "{\n.reg .pred P1;\nWAIT_R%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n"
-        "@!P1 bra WAIT_R%=;\n}\n" ::"r"(msmem_u32(&bar))
-        : "memory");
+    wait_rv();
 #pragma unroll
     for (int j = 0; j < HPT; ++j) acc[j] = 0.f;
     const float4* Rrow = reinterpret_cast<const float4*>(Rs + (size_t)cp * kD);
@@ -638,32 +731,22 @@ __global__ void __launch_bounds__(256) attend_segment_kernel(AttnParams p, const
 }
 
 // ------------------------------------------------------------------ host side
-// Pages per split (per work item).  Simple kernel: ~8 CTAs per SM over the grid.  Tensor-core
-// kernel: warp-granular items, ~3 per warp of a nominal 16-warps/SM residency, 8..32 pages.
-int attend_mma_total_warps(const oscar_ctx& c);                              // attend_mma.cu
-
-// Pages per split-K work item.  Tensor-core path: as few items as keep every warp of the
-// persistent grid busy — floor(warps / (B·H_kv)) splits per (sequence, kv head) — so each warp
-// gets one balanced item (≤ 64 pages: the partial kernel holds an item's page indices two per
-// lane); fewer, longer items also cut the split partials the merge reads.
+// Split-K granularity.
+// Tensor-core path (balanced decomposition, attend_mma.cu): every warp of the persistent grid gets
+// an equal contiguous range of the call's page-heads, at least pmin pages long; pmin bounds the
+// split slots a unit can need: <= ceil(max_pages / pmin) + 2 (pmin = attend_pages_per_split when
+// set, else the smallest value >= 4 that keeps the slots <= 64).
+static int mma_pmin(const oscar_ctx& c, int max_pages) {
+  if (c.pages_per_split > 0) return c.pages_per_split;
+  const int pm = (max_pages + 61) / 62;
+  return pm < 4 ? 4 : pm;
+}
+// CUDA-core kernel (variant 1, b = 3): pages per split of a (split, kv head, sequence) grid with
+// ~8 resident CTAs per SM; aim at ~8 waves of short splits (at least 4 pages) so the last wave is
+// a small fraction of the kernel (3-bit C2 shape: 52 -> 7 pages per split, 1.00 -> 0.81 ms)
 static int choose_pps(const oscar_ctx& c, int B, int max_pages) {
+  if (c.pages_per_split > 0) return c.pages_per_split;
   const long units = (long)B * c.hkv;
-  const bool mma = c.variant == 0 && attend_mma_supported(c);
-  if (c.pages_per_split > 0) return (mma && c.pages_per_split > 64) ? 64 : c.pages_per_split;
-  if (mma) {
-    const long warps = attend_mma_total_warps(c);
-    long splits = units > 0 ? warps / units : 1;
-    if (splits < 1) splits = 1;
-    long pps = (max_pages + splits - 1) / splits;
-    const long lo = max_pages < 4 ? (max_pages > 0 ? max_pages : 1) : 4;
-    // one wave of items of up to 64 pages when that covers the cache; otherwise items of at most
-    // 32 pages, several per warp from the work counter (short items keep the last wave short)
-    pps = pps < lo ? lo : (pps > 64 ? 32 : pps);
-    return (int)pps;
-  }
-  // CUDA-core kernel: ~8 resident CTAs per SM; aim at ~8 waves of short splits (at least 4
-  // pages) so the last wave is a small fraction of the kernel (3-bit C2 shape: 52 -> 7 pages
-  // per split, 1.00 -> 0.81 ms)
   const long target = (long)c.num_sms * 64;
   long splits = (target + units - 1) / units;
   if (splits < 1) splits = 1;
@@ -672,6 +755,15 @@ static int choose_pps(const oscar_ctx& c, int B, int max_pages) {
   const long lo = max_pages < 4 ? (max_pages > 0 ? max_pages : 1) : 4;
   return (int)(pps < lo ? lo : pps);
 }
+// split slots per (sequence, query head) in the workspace
+static int n_split_slots(const oscar_ctx& c, int B, int max_pages) {
+  if (c.variant == 0 && attend_mma_supported(c)) {
+    const int pm = mma_pmin(c, max_pages);
+    return (max_pages + pm - 1) / pm + 2;
+  }
+  const int pps = choose_pps(c, B, max_pages);
+  return (max_pages + pps - 1) / pps;
+}
 
 // Workspace carve-up: every sub-buffer starts on a 256-B boundary (the kernels use 8- and 16-B
 // vector accesses on them, and B·H_q may be odd).
@@ -679,8 +771,7 @@ struct WsLayout {
   size_t qt, ws_o, ws_m, ws_l, qsum, qscale, qint, qfrag, work, seg_o, seg_m, seg_l, total;
 };
 static WsLayout ws_layout(const oscar_ctx& c, int B, int max_pages) {
-  const int pps = choose_pps(c, B, max_pages);
-  const size_t ns = (size_t)((max_pages + pps - 1) / pps);
+  const size_t ns = (size_t)n_split_slots(c, B, max_pages);
   const size_t rows = (size_t)B * c.hq;
   const size_t nt = (size_t)((c.g * c.ng + 7) / 8);
   WsLayout w{};
@@ -710,7 +801,6 @@ size_t attend_workspace_bytes(const oscar_ctx& c, int B, int max_pages) {
   return ws_layout(c, B, max_pages).total;
 }
 
-cudaError_t launch_attend_mma(const AttnParams& p, int total_warps, cudaStream_t s);
 
 cudaError_t launch_attend(const oscar_ctx& c, const void* q, const int32_t* page_table,
                           const int32_t* seq_lens, int B, int max_pages, const void* pool,
@@ -722,12 +812,17 @@ cudaError_t launch_attend(const oscar_ctx& c, const void* q, const int32_t* page
   p.hq = c.hq; p.hkv = c.hkv; p.g = c.g; p.P = c.P; p.bits = c.bits; p.G = c.G; p.ng = c.ng;
   p.row_bytes = c.row_bytes; p.vcodes_off = c.vcodes_off; p.meta_off = c.meta_off;
   p.page_bytes = c.page_bytes; p.max_pages = max_pages;
-  p.pps = choose_pps(c, B, max_pages);
-  p.n_splits = (max_pages + p.pps - 1) / p.pps;
+  p.n_splits = n_split_slots(c, B, max_pages);
+  if (mma) {
+    p.balanced = 1;
+    p.pmin = mma_pmin(c, max_pages);
+    p.n_warps = attend_mma_total_warps(c, B);
+  } else {
+    p.pps = choose_pps(c, B, max_pages);
+  }
   p.page_table = page_table; p.seq_lens = seq_lens;
   p.pool = static_cast<const uint8_t*>(pool);
   p.nt = (c.g * c.ng + 7) / 8;
-  p.n_items = B * c.hkv * p.n_splits;
   p.batch = B;
   // workspace carve-up (ws_layout: 256-B aligned sub-buffers)
   {
@@ -757,27 +852,32 @@ cudaError_t launch_attend(const oscar_ctx& c, const void* q, const int32_t* page
   cudaError_t e = cudaSuccess;
   {
     PrologueParams pp{};
-    pp.q = static_cast<const uint16_t*>(q); pp.RK = RK; pp.RV = RV;
+    pp.q = static_cast<const uint16_t*>(q); pp.RK = RK;
     pp.Hq = c.hq; pp.lgG = lgG; pp.bits = c.bits; pp.nt = p.nt; pp.qscale = c.scale * kLog2e;
     pp.qt = p.qt; pp.qint = p.qint; pp.qsc = p.qscale; pp.qsum = p.qsum;
     pp.qfrag = mma ? p.qfrag : nullptr;
     pp.tq = mma && attend_mma_tq(c) ? 1 : 0; pp.work = mma ? p.work : nullptr;
-    pp.knew = static_cast<const uint16_t*>(k_new); pp.vnew = static_cast<const uint16_t*>(v_new);
-    pp.page_table = page_table; pp.seq_lens = seq_lens; pp.max_pages = max_pages;
-    pp.pool = static_cast<uint8_t*>(const_cast<void*>(pool));
-    pp.ep = make_epi_params(c);
     void (*fn)(PrologueParams) = c.g == 1 ? attend_prologue_kernel<1> : c.g == 2 ? attend_prologue_kernel<2>
                                : c.g == 4 ? attend_prologue_kernel<4> : attend_prologue_kernel<8>;
-    const int psmem = 16 * (c.g + 2) * kD * (int)sizeof(float);
+    const int psmem = 16 * c.g * kD * (int)sizeof(float);
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, psmem);
     if (e != cudaSuccess) return e;
-    // an ordinary launch (not PDL): every earlier kernel of the stream has completed when it
-    // starts, so the partial kernel's early page prefetch never races the caller's writes
-    fn<<<dim3(B, c.hkv), 512, psmem, s>>>(pp);
-    e = cudaGetLastError();
+    // PDL launch: its CTAs may become resident while the previous kernel of the stream drains;
+    // the kernel's first instruction waits for that kernel's completion, so every later read
+    // (and the partial kernel's early page prefetch) sees the caller's writes
+    cudaLaunchConfig_t pcfg{};
+    pcfg.gridDim = dim3((unsigned)B, (unsigned)c.hkv);
+    pcfg.blockDim = dim3(512);
+    pcfg.dynamicSmemBytes = psmem;
+    pcfg.stream = s;
+    pcfg.attrs = pdl;
+    pcfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&pcfg, fn, pp);
     if (e != cudaSuccess) return e;
   }
-  p.protect_last = k_new != nullptr;
+  // decode step: the partial kernels attend over the first seq_len - 1 tokens; the merge kernel
+  // appends the new row and folds it in as one more partial (attend_merge_kernel)
+  p.len_adj = k_new != nullptr ? 1 : 0;
   if (!mma) {
     const int smem = (8 * kD + 64 + 8 * c.P + 24) * 4 + ((c.page_bytes + 15) & ~15) + c.P * (kD / c.G) * 8;
 #define OSCAR_SIMPLE(BB) (c.g == 1 ? attend_partial_simple<BB, 1> : c.g == 2 ? attend_partial_simple<BB, 2> \
@@ -788,7 +888,7 @@ cudaError_t launch_attend(const oscar_ctx& c, const void* q, const int32_t* page
     if (e != cudaSuccess) return e;
     sfn<<<dim3(p.n_splits, c.hkv, B), 128, smem, s>>>(p);
   } else {
-    e = launch_attend_mma(p, attend_mma_total_warps(c), s);
+    e = launch_attend_mma(p, s);
     if (e != cudaSuccess) return e;
   }
   e = cudaGetLastError();
@@ -806,12 +906,17 @@ cudaError_t launch_attend(const oscar_ctx& c, const void* q, const int32_t* page
   {
     // small batches: one CTA per query head (the fold of many splits gets 8 warps per head)
     const bool per_head = (long)B * c.hkv * 4 <= (long)c.num_sms;
-    void (*fn)(AttnParams, const float*, void*, int, float*) =
+    void (*fn)(AttnParams, const float*, void*, int, float*, StepParams) =
         per_head ? attend_merge_kernel<1>
       : c.g == 1 ? attend_merge_kernel<1> : c.g == 2 ? attend_merge_kernel<2>
       : c.g == 4 ? attend_merge_kernel<4> : attend_merge_kernel<8>;
     const int hc = per_head ? 1 : c.g;
     const int msmem = RV ? kD * kD * 4 : 0;
+    StepParams sp{};
+    sp.knew = static_cast<const uint16_t*>(k_new); sp.vnew = static_cast<const uint16_t*>(v_new);
+    sp.RK = RK; sp.page_table = page_table; sp.seq_lens = seq_lens; sp.max_pages = max_pages;
+    sp.pool = static_cast<uint8_t*>(const_cast<void*>(pool));
+    sp.ep = make_epi_params(c);
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, msmem);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg{};
@@ -821,7 +926,7 @@ cudaError_t launch_attend(const oscar_ctx& c, const void* q, const int32_t* page
     cfg.stream = s;
     cfg.attrs = pdl;
     cfg.numAttrs = OSCAR_PDL_MERGE;
-    e = cudaLaunchKernelEx(&cfg, fn, p, RV, out, out_fp32, lse);
+    e = cudaLaunchKernelEx(&cfg, fn, p, RV, out, out_fp32, lse, sp);
     if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();

@@ -21,16 +21,20 @@ struct AttnParams {
   uint32_t* qfrag;             // [B][H_kv][NT*16][32] IMMA A fragments (hi/lo int8 of qint)
   int32_t* work;               // work-item counter of the persistent partial kernel
   int nt;                      // ceil(g * ng / 8)
-  int n_items;                 // B * H_kv * n_splits
+  int balanced;                // 1: tensor-core partial kernel's balanced decomposition (n_splits =
+                               //    split slots per unit; the merge recomputes each unit's count)
+  int n_warps, pmin;           // balanced: warps of the persistent grid, minimum pages per warp
   // optional bf16 segment (sink + recent window, NEXT-1): partial in the ORIGINAL frame
   float* seg_o;                // [B][H_q][128] unnormalized Σ p v (null: no segment)
   float* seg_m;                // [B][H_q]
   float* seg_l;                // [B][H_q]
-  int protect_last;            // decode step: the prologue writes each sequence's last page, so
-                               // the partial kernel loads it only after griddepcontrol.wait
+  int len_adj;                 // decode step: 1 (the partial kernels attend over seq_len - 1
+                               // tokens; the merge kernel appends and folds the new token)
 };
 
 bool attend_mma_supported(const oscar_ctx& c);
+int attend_mma_total_warps(const oscar_ctx& c, int B);
+cudaError_t launch_attend_mma(const AttnParams& p, cudaStream_t s);
 bool attend_mma_tq(const oscar_ctx& c);      // the partial kernel uses the token-row QK layout
 
 // IMMA QK k-slot -> channel map (see attend_mma.cu): in K-step kk (0..3), lane t's B

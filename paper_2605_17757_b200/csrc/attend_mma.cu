@@ -3,11 +3,12 @@
 // Attention Kernel" (unpack bytes, apply the stored scale/zero, accumulate in
 // floating point; split-K partials merged with online softmax by attend_merge_kernel).
 //
-// Persistent, warp-granular: every warp is an independent worker that pulls work items
-// (sequence b, kv head h, split of `pps` pages) from an atomic counter and streams the
-// items' 5120-B page blocks through a private smem ring with cp.async.bulk + mbarrier
-// (evict-first L2 policy; the next item's first pages are prefetched while the current one
-// finishes).  Per page, in chunks of up to 64 tokens:
+// Persistent, warp-granular: every warp of the (fully resident) grid takes one KV head of an
+// equal contiguous range of the call's pages (balanced decomposition, struct Decomp: a range
+// may span sequences, each (sequence, head) piece is one split partial) and
+// streams its 5120-B page blocks through a private smem ring with cp.async.bulk + mbarrier
+// (evict-first L2 policy; prefetch runs across unit boundaries).  Per page, in chunks of up to
+// 64 tokens:
 //   QK  : IMMA m16n8k32 s8 x u8 -> s32.  A = q̃ quantized to 15 bits and split hi/lo int8
 //         (rows = (hi|lo) x (group, head) "combos", zero outside the combo's group; built once
 //         per (b, h) by attend_prologue_kernel), B = the raw 2/4-bit codes moved to the top bits of
@@ -144,18 +145,29 @@ struct Item {
   int b, h, split, page0, np, seq_len;
 };
 
-__device__ __forceinline__ Item decode_item(const AttnParams& p, int it) {
-  Item I;
-  I.split = it % p.n_splits;
-  const int bh = it / p.n_splits;
-  I.h = bh % p.hkv;
-  I.b = bh / p.hkv;
-  I.seq_len = p.seq_lens[I.b];
-  I.page0 = I.split * p.pps;
-  const int npg = (I.seq_len + p.P - 1) / p.P;
-  I.np = max(0, min(p.pps, npg - I.page0));
-  return I;
-}
+// Balanced work decomposition: the pages of all sequences, in sequence order
+// (sequence b has npg(b) = ceil(len_b / P) pages), are cut into Wr equal contiguous ranges; warp
+// gw takes range gw / H_kv for KV head gw % H_kv, so the H_kv warps of a range read the same
+// physical pages (heads side by side in the pool) at the same time.  A range may span sequences;
+// each (sequence, head) piece is one split partial.  pre[b] = Σ_{b' < b} npg(b') (CTA shared
+// memory).  The range holding sequence page x is rof(x) = ⌊((x + 1)·Wr − 1) / T⌋; the piece of
+// range r goes to split slot r − rof(pre[b]), which the merge kernel recomputes.
+struct Decomp {
+  const int* pre;
+  int B;
+  int64_t T, W;        // pages of all sequences, ranges
+  __device__ __forceinline__ int64_t rof(int64_t x) const { return ((x + 1) * W - 1) / T; }
+  // sequence b and page k of sequence page x
+  __device__ __forceinline__ void locate(int64_t x, int& b, int& k) const {
+    int l = 0, r = B;
+    while (r - l > 1) {
+      const int m = (l + r) >> 1;
+      if (pre[m] <= x) l = m; else r = m;
+    }
+    b = l;
+    k = (int)(x - pre[l]);
+  }
+};
 
 }  // namespace
 
@@ -203,47 +215,62 @@ attend_partial_mma(AttnParams p, int S) {
   uint64_t policy;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(policy));
 
-  // work items: the first two per warp are static (no atomic latency at start), the rest are
-  // pulled from the counter (reset to 0 by attend_prologue_kernel) offset by 2·(total warps)
-  const int n_items = p.n_items;
-  const int total_warps = gridDim.x * kWarps, gw = blockIdx.x * kWarps + warp;
-  auto fetch_async = [&]() { return lane == 0 ? atomicAdd(p.work, 1) + 2 * total_warps : 0; };
-  auto bcast = [&](int v) { return __shfl_sync(0xffffffffu, v, 0); };
-  int cur = gw, nxt = gw + total_warps;
-  // loader view of an item: pages, kv head; lane l holds the item's page indices l and 32 + l
-  // (pps <= 64)
-  int cur_np = 0, cur_h = 0, pidx_cur = 0, pidx_cur2 = 0, nxt_np = 0, nxt_h = 0, pidx_nxt = 0, pidx_nxt2 = 0;
-  int cur_last = -1, nxt_last = -1;   // local index of the sequence's last page in the item, or -1
-  auto load_item = [&](int it, int& np, int& h, int& pidx, int& pidx2, int& last) {
-    np = 0; h = 0; pidx = 0; pidx2 = 0; last = -1;
-    if (it < n_items) {
-      const Item L = decode_item(p, it);
-      np = L.np; h = L.h;
-      if (np > 0 && L.page0 + np == (L.seq_len + p.P - 1) / p.P) last = np - 1;
-      const int32_t* row = p.page_table + (size_t)L.b * p.max_pages + L.page0;
-      if (lane < L.np) pidx = row[lane];
-      if (32 + lane < L.np) pidx2 = row[32 + lane];
+  // ---- balanced decomposition: prefix of pages per sequence (warp 0), then this warp's range
+  int* pre = reinterpret_cast<int*>(smem + (size_t)kWarps * S * (page_bytes + 8));
+  if (warp == 0) {
+    int run = 0;
+    for (int b0 = 0; b0 < p.batch; b0 += 32) {
+      const int bb = b0 + lane;
+      const int n = bb < p.batch ? (max(p.seq_lens[bb] - p.len_adj, 0) + P - 1) / P : 0;
+      int inc = n;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      if (bb < p.batch) pre[bb] = run + inc - n;
+      run += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    if (lane == 0) pre[p.batch] = run;
+  }
+  __syncthreads();
+  Decomp dc;
+  dc.pre = pre; dc.B = p.batch;
+  dc.T = pre[p.batch];
+  dc.W = min((int64_t)(p.n_warps / p.hkv), max((int64_t)1, dc.T / p.pmin));
+  const int gw = blockIdx.x * kWarps + warp;
+  const int rng = gw / p.hkv, my_h = gw - rng * p.hkv;
+  const int64_t lo = rng < dc.W ? (int64_t)rng * dc.T / dc.W : dc.T;
+  const int64_t hi = rng < dc.W ? (int64_t)(rng + 1) * dc.T / dc.W : dc.T;
+  const int64_t nstream = hi - lo;
+  // loader: page indices of stream positions [wb, wb + 32) in window c, [wb + 32, wb + 64) in
+  // window n, one per lane; the next window is loaded 32 pages ahead of its use
+  int pid_c = 0, pid_n = 0, wb = 0;
+  auto load_window = [&](int base, int& pid) {
+    pid = 0;
+    const int64_t x = lo + base + lane;
+    if (x < hi) {
+      int bb, kx;
+      dc.locate(x, bb, kx);
+      pid = p.page_table[(size_t)bb * p.max_pages + kx];
     }
   };
-  load_item(cur, cur_np, cur_h, pidx_cur, pidx_cur2, cur_last);
-  load_item(nxt, nxt_np, nxt_h, pidx_nxt, pidx_nxt2, nxt_last);
-  // loader: `lq` = stream position of the next page to issue, counted from cur's first page
-  // (pages past cur's end belong to nxt); stages are used in order, one mbarrier each.
-  // Before griddepcontrol.wait (decode step) a sequence's last page is not loaded: the
-  // prologue kernel may still be appending the step's row to it.
+  load_window(0, pid_c);
+  load_window(32, pid_n);
+  // stages are used in order, one mbarrier each.  (Pages are only read by this call until the
+  // merge kernel, which appends the decode step's row, so every page may be prefetched before
+  // griddepcontrol.wait.)
   int lq = 0, s_issue = 0, inflight = 0;
-  bool waited = false;
   auto issue_one = [&]() -> bool {
-    const bool in_cur = lq < cur_np;
-    const int kn = lq - cur_np;
-    if (!in_cur && kn >= nxt_np) return false;
-    if (!waited && p.protect_last && (in_cur ? lq == cur_last : kn == nxt_last)) return false;
-    const int li = in_cur ? lq : kn;
-    const int64_t page = __shfl_sync(0xffffffffu, in_cur ? (li < 32 ? pidx_cur : pidx_cur2)
-                                                         : (li < 32 ? pidx_nxt : pidx_nxt2), li & 31);
-    const int h = in_cur ? cur_h : nxt_h;
+    if (lq >= nstream) return false;
+    if (lq - wb >= 32) {                       // window c exhausted: shift, prefetch the next
+      pid_c = pid_n; wb += 32;
+      load_window(wb + 32, pid_n);
+    }
+    const int li = lq - wb;
+    const int64_t page = __shfl_sync(0xffffffffu, pid_c, li);
     if (lane == 0)
-      bulk_load(ring + (size_t)s_issue * page_bytes, p.pool + (page * p.hkv + h) * (int64_t)page_bytes,
+      bulk_load(ring + (size_t)s_issue * page_bytes, p.pool + (page * p.hkv + my_h) * (int64_t)page_bytes,
                 page_bytes, &bars[s_issue], policy);
     s_issue = s_issue + 1 == S ? 0 : s_issue + 1;
     ++lq;
@@ -253,17 +280,25 @@ attend_partial_mma(AttnParams p, int S) {
   // the first pages depend only on the caller's inputs: start streaming before the prologue ends
   while (inflight < S && issue_one()) {}
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
-  waited = true;
   while (inflight < S && issue_one()) {}
-  int pending = nxt < n_items ? fetch_async() : 0;   // the item after nxt (broadcast when needed)
 
   const int hh = gid % GQ;                    // every tile of this lane serves head hh
   const bool real = NC >= 8 || gid < NC;
   int s_use = 0;
   uint32_t ph_use = 0;
 
-  while (cur < n_items) {
-    const Item I = decode_item(p, cur);
+  for (int64_t x = lo; x < hi;) {
+    Item I;
+    {
+      int kx;
+      dc.locate(x, I.b, kx);
+      I.h = my_h;
+      I.page0 = kx;
+      I.np = (int)min((int64_t)(pre[I.b + 1] - pre[I.b] - kx), hi - x);
+      I.seq_len = max(p.seq_lens[I.b] - p.len_adj, 0);
+      I.split = (int)(rng - dc.rof(pre[I.b]));
+      x += I.np;
+    }
     const size_t qrow = (size_t)I.b * p.hq + (size_t)I.h * GQ + hh;
     constexpr float kBScale = (float)(1 << (8 - BITS));   // B bytes carry c·2^(8-BITS)
     const float qscale = real ? p.qscale[qrow] * (1.f / kBScale) : 0.f;
@@ -815,14 +850,6 @@ attend_partial_mma(AttnParams p, int S) {
       p.ws_m[row] = I.np > 0 ? m_run : -INFINITY;
       p.ws_l[row] = l_run;
     }
-    // ---- advance: the loader already moved on to `nxt`
-    lq -= cur_np;
-    cur = nxt;
-    cur_np = nxt_np; cur_h = nxt_h; pidx_cur = pidx_nxt; pidx_cur2 = pidx_nxt2; cur_last = nxt_last;
-    nxt = cur < n_items ? bcast(pending) : n_items;
-    load_item(nxt, nxt_np, nxt_h, pidx_nxt, pidx_nxt2, nxt_last);
-    pending = nxt < n_items ? fetch_async() : 0;
-    while (inflight < S && issue_one()) {}
   }
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");   // let the merge kernel launch
 }
@@ -878,15 +905,21 @@ bool attend_mma_supported(const oscar_ctx& c) {
   return c.d == 128 && pick(c.bits, c.g, c.ng) != nullptr && c.P % 16 == 0 && stages_for(c.page_bytes) > 0;
 }
 
-int attend_mma_total_warps(const oscar_ctx& c) {
+// dynamic smem of the partial kernel: per-warp page rings + their mbarriers + the CTA's page
+// prefix pre[B + 1] (balanced decomposition)
+static int mma_smem(int page_bytes, int B) {
+  return kWarps * stages_for(page_bytes) * (page_bytes + 8) + ((B + 1) * 4 + 15) / 16 * 16;
+}
+
+// Warps of the persistent grid: SMs x resident CTAs per SM x 4 (every CTA resident at once)
+int attend_mma_total_warps(const oscar_ctx& c, int B) {
   KernelFn fn = pick(c.bits, c.g, c.ng);
   if (!fn) return 0;
-  const int S = stages_for(c.page_bytes);
-  const int smem = kWarps * S * (c.page_bytes + 8);
+  const int smem = mma_smem(c.page_bytes, B);
   // resident CTAs per SM, cached per (kernel, smem): the query is a few µs of host time
   // (contexts may be used from several host threads: the cache is guarded)
   static std::mutex mu;
-  static struct { KernelFn fn; int smem, per_sm; } cache[16];
+  static struct { KernelFn fn; int smem, per_sm; } cache[64];
   std::lock_guard<std::mutex> lock(mu);
   for (auto& e : cache)
     if (e.fn == fn && e.smem == smem) return c.num_sms * e.per_sm * kWarps;
@@ -902,15 +935,14 @@ int attend_mma_total_warps(const oscar_ctx& c) {
   return c.num_sms * per_sm * kWarps;
 }
 
-cudaError_t launch_attend_mma(const AttnParams& p, int total_warps, cudaStream_t s) {
+cudaError_t launch_attend_mma(const AttnParams& p, cudaStream_t s) {
   KernelFn fn = pick(p.bits, p.g, p.ng);
   if (!fn) return cudaErrorNotSupported;
   const int S = stages_for(p.page_bytes);
-  const int smem = kWarps * S * (p.page_bytes + 8);
+  const int smem = mma_smem(p.page_bytes, p.batch);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  int warps = total_warps < p.n_items ? total_warps : p.n_items;
-  const int grid = (warps + kWarps - 1) / kWarps;
+  const int grid = p.n_warps / kWarps;
   // programmatic dependent launch: the first page loads overlap attend_prologue_kernel;
   // griddepcontrol.wait in the kernel orders every read of the prologue's outputs
   cudaLaunchConfig_t cfg{};

@@ -97,8 +97,7 @@ def test_decode_step_parity(cfg, variant, prerot_v):
 
 
 def test_decode_step_equals_append_then_attend():
-    """The fused call and the two-call sequence (quantize_append, then attend) agree: identical
-    outputs wherever the two paths' fp32 rotations round the new row's codes the same way."""
+    """The fused call and the two-call sequence (quantize_append, then attend) agree."""
     import torch
     rng = np.random.default_rng(11)
     Hq, Hkv, B, L = 32, 8, 4, [640, 1000, 64, 65]
@@ -129,10 +128,9 @@ def test_decode_step_equals_append_then_attend():
     for p_ in (p1, p2):                      # both pools: oracle up to validated boundary flips
         check_step_pool(p_.cpu().numpy(), pool_ref_after(pool, pt, L, k_new, v_new, RK, RV, fmt), pt, L,
                         k_new, v_new, RK, RV, fmt, list(range(B)))
-    if torch.equal(p1, p2):
-        assert torch.equal(o1, o2)
-    else:
-        assert (o1 - o2).abs().max().item() <= 2e-3
+    # the fused step folds the new token as its own partial (fp32 logit q̃·k̂), the two-call path
+    # through the IMMA kernel (15-bit q̃, reading Z31): equal up to that rounding
+    assert (o1 - o2).abs().max().item() <= (2e-4 if torch.equal(p1, p2) else 2e-3)
 
 
 def pool_ref_after(pool, pt, L, k_new, v_new, RK, RV, fmt):

@@ -4,6 +4,8 @@ seq_lens[b] tokens including it (reading Z20).  The oracle runs the same two ste
 quantize_append and attend on the same seeded inputs.  Bars as test_gpu_parity.py: pool bytes
 equal except rounding-boundary flips of the fp32 rotation, outputs within 2e-3 max-abs (fp32
 output mode), lse within the IMMA path's 15-bit q̃ bound."""
+import zlib
+
 import numpy as np
 import pytest
 
@@ -52,7 +54,7 @@ def check_step_pool(got_pool, ref_pool, pt, L, k_new, v_new, RK, RV, fmt, live, 
 @pytest.mark.parametrize("prerot_v", [False, True])
 def test_decode_step_parity(cfg, variant, prerot_v):
     import torch
-    rng = np.random.default_rng(abs(hash((cfg["name"], variant, prerot_v))) % 2 ** 31)
+    rng = np.random.default_rng(zlib.crc32(f"{cfg['name']}/{variant}/{prerot_v}".encode()))
     Hq, Hkv, L = cfg["Hq"], cfg["Hkv"], cfg["L"]
     B = len(L)
     fmt = O.PageFormat(128, cfg["bits"], cfg["G"], 64)

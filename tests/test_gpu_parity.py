@@ -9,6 +9,7 @@ inputs.  Tolerances (north star):
     RNE(fp32 mode) bit-for-bit (reading Z25)
 """
 import math
+import zlib
 
 import numpy as np
 import pytest
@@ -240,6 +241,26 @@ def _run_attend(o, q, pt, L, pool, RK, RV):
     return out32, out16, lse
 
 
+def _z31_lse_bound(q, pt, L, pool, RK, fmt, Hkv):
+    """Reading Z31: the tensor-core path rounds q̃ = q·R_K·scale·log2(e) to integers of step
+    qscale = max|q̃| / 32639, so every logit (log2 units) moves by at most (qscale / 2)·‖k̂_t‖₁
+    and so does log2 Σ 2^logit; in natural-log units x ln 2.  Per (sequence, query head)."""
+    B, Hq, d = q.shape
+    g = Hq // Hkv
+    out = np.zeros((B, Hq))
+    for b in range(B):
+        if L[b] == 0:
+            continue
+        slots = np.asarray(pt[b], np.int64)[np.arange(L[b]) // fmt.P] * fmt.P + np.arange(L[b]) % fmt.P
+        for h in range(Hkv):
+            Kh, _ = O.read_rows(pool, slots, h, fmt)
+            k1 = np.abs(Kh).sum(axis=1).max()
+            for i in range(h * g, (h + 1) * g):
+                qt = np.asarray(q[b, i], np.float64) @ RK[h] / math.sqrt(d) * math.log2(math.e)
+                out[b, i] = math.log(2) * 0.5 * np.abs(qt).max() / 32639 * k1
+    return out
+
+
 @pytest.mark.parametrize("cfg", [
     dict(name="C1", Hq=1, Hkv=1, bits=4, G=32, B=64, L="ramp256"),
     dict(name="C2small", Hq=32, Hkv=8, bits=2, G=64, B=3, L=[1000, 77, 0]),
@@ -258,7 +279,7 @@ def _run_attend(o, q, pt, L, pool, RK, RV):
 @pytest.mark.parametrize("qsig", [2.0, 8.0])          # 8.0: the "peaky" decode q
 def test_attend_parity(cfg, variant, pps, qsig):
     torch = _torch()
-    rng = np.random.default_rng(hash(cfg["name"]) % 2 ** 31)
+    rng = np.random.default_rng(zlib.crc32(cfg["name"].encode()))    # stable across processes
     fmt = O.PageFormat(128, cfg["bits"], cfg["G"], 64)
     L = list(range(4, 260, 4)) if cfg["L"] == "ramp256" else cfg["L"]
     B = cfg["B"]
@@ -276,8 +297,9 @@ def test_attend_parity(cfg, variant, pps, qsig):
     lg = lse.cpu().numpy()
     fin = np.isfinite(ref_lse)
     assert np.array_equal(np.isfinite(lg), fin)
-    # lse: the IMMA path quantizes q̃ to 15 bits (reading Z31): logit error <= ~1e-4 relative
-    assert (np.abs(lg[fin] - ref_lse[fin]) <= 1e-3 + 1e-4 * np.abs(ref_lse[fin])).all()
+    # lse: the IMMA path quantizes q̃ to 15 bits (reading Z31); the bound of that reading per row
+    bound = _z31_lse_bound(q, pt, L, pool, RK, fmt, cfg["Hkv"]) + 1e-4 * np.abs(ref_lse) + 1e-4
+    assert (np.abs(lg[fin] - ref_lse[fin]) <= bound[fin]).all()
 
 
 @pytest.mark.parametrize("P,bits,G,Hq,Hkv", [(32, 2, 64, 32, 8), (128, 2, 64, 32, 8), (16, 2, 128, 16, 2),

@@ -6,8 +6,6 @@
 //                          (split, kv head, sequence)); the tensor-core kernel is in
 //                          attend_mma.cu (variant 0)
 //   attend_merge_kernel    LSE merge over splits, o = õ · R_Vᵀ, bf16/fp32 store, lse
-#include <cstdio>
-#include <cstdlib>
 #include <type_traits>
 #include "common.cuh"
 #include "attend_common.cuh"
@@ -47,7 +45,6 @@ struct PrologueParams {
   uint32_t* qfrag;              // null: simple kernel path
   int tq;                       // 1: fragments for the token-row QK layout of attend_partial_mma
   int32_t* work;                // null: simple kernel path
-  int work_n;                   // ints of `work` to zero (attend_common.cuh work_ints)
   unsigned long long* tl;       // timing probe (OSCAR_PROBE_TL)
 };
 
@@ -68,9 +65,7 @@ __global__ void __launch_bounds__(512) attend_prologue_kernel(PrologueParams pp)
   const int b = blockIdx.x, h = blockIdx.y, tid = threadIdx.x;
   const int w = tid >> 5, lane = tid & 31;
   const int G = 1 << pp.lgG;
-  // zero the partial kernel's arrival counters (its CTAs take them after griddepcontrol.wait)
-  if (pp.work && b == 0 && h == 0)
-    for (int i = tid; i < pp.work_n; i += 512) pp.work[i] = 0;
+  if (pp.work && b == 0 && h == 0 && tid == 0) *pp.work = 0;   // reset the work-item counter
 #ifdef OSCAR_PROBE_NOPRO
   return;                                            // timing probe only (results invalid)
 #endif
@@ -548,8 +543,10 @@ __global__ void __launch_bounds__(256) attend_merge_kernel(AttnParams p, const f
 #pragma unroll
     for (int i = 0; i < 8; ++i) { lt += red[0][i]; tot += red[1][i]; }
     const int npg = (max(p.seq_lens[b] - p.len_adj, 0) + p.P - 1) / p.P;
-    const RangeMap rm = make_range_map(p, tot);
-    ns = npg > 0 ? (int)(rm.rof(lt + npg - 1) - rm.rof(lt) + 1) : 0;
+    const int64_t T = tot;
+    const int64_t W = min((int64_t)(p.n_warps / p.hkv), max((int64_t)1, T / p.pmin));
+    auto rof = [&](int64_t x) { return ((x + 1) * W - 1) / T; };
+    ns = npg > 0 ? (int)(rof(lt + npg - 1) - rof(lt) + 1) : 0;
   }
   if (tid == 0) tl_mark(p.tl, 2, tl_idx, 1);
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
@@ -748,21 +745,6 @@ __global__ void __launch_bounds__(256) attend_segment_kernel(AttnParams p, const
 // an equal contiguous range of the call's page-heads, at least pmin pages long; pmin bounds the
 // split slots a unit can need: <= ceil(max_pages / pmin) + 2 (pmin = attend_pages_per_split when
 // set, else the smallest value >= 4 that keeps the slots <= 64).
-// Range weights by warp-slot quarter on the SM (RangeMap, attend_common.cuh).  Measured on B200
-// at the C2 decode step (tools/timeline_probe.py, equal weights, 4 CTAs x 4 warps per SM): the
-// CTAs in slots 0-3 / 4-7 / 8-11 / 12-15 streamed for 58.4 / 63.0 / 68.3 / 74.1 µs; the weight
-// is the inverse.  OSCAR_RANGE_WEIGHTS="a,b,c,d" overrides (probes).
-static void range_weights(int per_sm, int* w) {
-  static int env[4] = {0, 0, 0, 0};
-  static const bool have_env = [] {
-    const char* e = getenv("OSCAR_RANGE_WEIGHTS");
-    return e && sscanf(e, "%d,%d,%d,%d", &env[0], &env[1], &env[2], &env[3]) == 4;
-  }();
-  static const int w4[4] = {1400, 1270, 1130, 1000};
-  static const int w3[4] = {1000, 1000, 1000, 1000};
-  for (int q = 0; q < 4; ++q) w[q] = have_env ? env[q] : (per_sm >= 4 ? w4[q] : w3[q]);
-}
-
 static int mma_pmin(const oscar_ctx& c, int max_pages) {
   if (c.pages_per_split > 0) return c.pages_per_split;
   const int pm = (max_pages + 61) / 62;
@@ -816,7 +798,7 @@ static WsLayout ws_layout(const oscar_ctx& c, int B, int max_pages) {
   w.qscale = take(rows * 4);
   w.qint = take(rows * kD * 2);
   w.qfrag = take((size_t)B * c.hkv * nt * 16 * 32 * 4);
-  w.work = take((size_t)work_ints(c.num_sms) * 4);
+  w.work = take(64 * 4);
   w.seg_o = take(rows * kD * 4);
   w.seg_m = take(rows * 4);
   w.seg_l = take(rows * 4);
@@ -851,10 +833,6 @@ cudaError_t launch_attend(const oscar_ctx& c, const void* q, const int32_t* page
     p.balanced = 1;
     p.pmin = mma_pmin(c, max_pages);
     p.n_warps = attend_mma_total_warps(c, B);
-    p.num_sms = c.num_sms;
-    p.cta_warps = attend_mma_cta_warps();
-    p.per_sm = p.n_warps / (p.cta_warps * c.num_sms);
-    range_weights(p.per_sm, p.rwts);
   } else {
     p.pps = choose_pps(c, B, max_pages);
   }
@@ -896,7 +874,6 @@ cudaError_t launch_attend(const oscar_ctx& c, const void* q, const int32_t* page
     pp.qt = p.qt; pp.qint = p.qint; pp.qsc = p.qscale; pp.qsum = p.qsum;
     pp.qfrag = mma ? p.qfrag : nullptr;
     pp.tq = mma && attend_mma_tq(c) ? 1 : 0; pp.work = mma ? p.work : nullptr;
-    pp.work_n = work_ints(c.num_sms);
     pp.tl = g_tl;
     void (*fn)(PrologueParams) = c.g == 1 ? attend_prologue_kernel<1> : c.g == 2 ? attend_prologue_kernel<2>
                                : c.g == 4 ? attend_prologue_kernel<4> : attend_prologue_kernel<8>;

@@ -30,59 +30,9 @@ struct AttnParams {
   float* seg_l;                // [B][H_q]
   int len_adj;                 // decode step: 1 (the partial kernels attend over seq_len - 1
                                // tokens; the merge kernel appends and folds the new token)
-  // rank-weighted decomposition of the tensor-core partial kernel (attend_mma.cu, RangeMap):
-  // per_sm CTAs resident on each of num_sms SMs, cta_warps warps each; zone q (the CTAs that
-  // arrived q-th on their SM) gets ranges weighted rwts[q]
-  int num_sms, per_sm, cta_warps, rwts[4];
   unsigned long long* tl;      // timing probe builds only (-DOSCAR_PROBE_TL): per-CTA/warp
                                // %globaltimer marks; null otherwise
 };
-
-// Layout of the `work` area of the workspace (ints): [0] unused, [1] arrivals, [2] overflow
-// count, [4 .. 64) bitmap of claimed virtual CTA slots (up to 1920).  Zeroed by the prologue
-// kernel before every partial kernel.
-__host__ __device__ __forceinline__ int work_ints(int) { return 64; }
-
-// Ranges of the rank-weighted balanced decomposition.  Warp issue priority on an SM falls with
-// the warp slot (measured, tools/timeline_probe.py: with equal ranges the CTAs in warp slots
-// 0-3 / 4-7 / 8-11 / 12-15 of an SM streamed for 58.4 / 63.0 / 68.3 / 74.1 µs, per-SM totals
-// equal), so the CTA in slots 4q..4q+3 takes a range of zone q, weighted w[q].  W ranges over T pages, per_zone ranges per zone; boundary(r) = ⌊S(r)·T / S(W)⌋ with S(r)
-// the summed weight of ranges 0..r-1; rof(x) = the range holding page x.  Shared by the partial
-// and the merge kernel so both see identical boundaries.
-struct RangeMap {
-  int64_t T, W;
-  int per_zone;
-  int w[4];
-  __host__ __device__ __forceinline__ int64_t S(int64_t r) const {
-    int64_t s = 0, b0 = 0;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int64_t b1 = q == 3 ? r : min(r, b0 + per_zone);
-      if (b1 > b0) s += (b1 - b0) * w[q];
-      b0 = b1 > b0 ? b1 : b0;
-    }
-    return s;
-  }
-  __host__ __device__ __forceinline__ int64_t boundary(int64_t r) const {
-    return r >= W ? T : S(r) * T / S(W);
-  }
-  __host__ __device__ __forceinline__ int64_t rof(int64_t x) const {   // largest r < W: boundary(r) <= x
-    int64_t l = 0, h = W;
-    while (h - l > 1) {
-      const int64_t m = (l + h) >> 1;
-      if (boundary(m) <= x) l = m; else h = m;
-    }
-    return l;
-  }
-};
-__host__ __device__ __forceinline__ RangeMap make_range_map(const AttnParams& p, int64_t T) {
-  RangeMap m;
-  m.T = T;
-  m.W = min((int64_t)(p.n_warps / p.hkv), max((int64_t)1, T / p.pmin));
-  m.per_zone = (p.num_sms * p.cta_warps + p.hkv - 1) / p.hkv;
-  for (int q = 0; q < 4; ++q) m.w[q] = q < p.per_sm ? p.rwts[q] : p.rwts[p.per_sm - 1];
-  return m;
-}
 
 // timeline probe (tools/timeline_probe.py): slot base of each kernel kind in the probe buffer
 __device__ __forceinline__ void tl_mark(unsigned long long* tl, int kind, int idx, int slot) {
@@ -97,7 +47,6 @@ __device__ __forceinline__ void tl_mark(unsigned long long* tl, int kind, int id
 
 bool attend_mma_supported(const oscar_ctx& c);
 int attend_mma_total_warps(const oscar_ctx& c, int B);
-int attend_mma_cta_warps();                   // warps per CTA of the partial kernel
 cudaError_t launch_attend_mma(const AttnParams& p, cudaStream_t s);
 bool attend_mma_tq(const oscar_ctx& c);      // the partial kernel uses the token-row QK layout
 

@@ -155,8 +155,8 @@ struct Item {
 struct Decomp {
   const int* pre;
   int B;
-  RangeMap rm;         // pages of all sequences, rank-weighted ranges (attend_common.cuh)
-  __device__ __forceinline__ int64_t rof(int64_t x) const { return rm.rof(x); }
+  int64_t T, W;        // pages of all sequences, ranges
+  __device__ __forceinline__ int64_t rof(int64_t x) const { return ((x + 1) * W - 1) / T; }
   // sequence b and page k of sequence page x
   __device__ __forceinline__ void locate(int64_t x, int& b, int& k) const {
     int l = 0, r = B;
@@ -214,48 +214,9 @@ attend_partial_mma(AttnParams p, int S) {
   __syncwarp();
   uint64_t policy;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(policy));
-  if (lane == 0) tl_mark(p.tl, 1, blockIdx.x * kWarps + warp, 0);
-  // the prologue kernel wrote q̃ and zeroed the arrival counters
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");
-  if (lane == 0) tl_mark(p.tl, 1, blockIdx.x * kWarps + warp, 1);
-
-  // ---- virtual CTA index v (RangeMap, attend_common.cuh).  Issue priority among the warps of
-  // an SM sub-partition falls with the warp slot, so a CTA whose warps sit in slots 4q..4q+3 of
-  // SM s (q = %warpid / 4 < per_sm, s = %smid < num_sms) takes v = q·num_sms + s, a range of zone
-  // q, claimed in a bitmap.  A CTA that finds no free slot that way (other kernels' warps holding
-  // low slots, more than per_sm CTAs on one SM over the launch) waits until every CTA has
-  // registered and takes the k-th unclaimed slot, so v is always a bijection onto the grid.
-  int* pre = reinterpret_cast<int*>(smem + (size_t)kWarps * S * (page_bytes + 8));
-  int* vslot = pre + p.batch + 1;
-  if (threadIdx.x == 0) {
-    unsigned smid, wid;
-    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
-    int v = -1;
-    const int q = (int)wid / kWarps;
-    if ((int)smid < p.num_sms && q < p.per_sm) {
-      const int cand = q * p.num_sms + (int)smid;
-      const unsigned bit = 1u << (cand & 31);
-      if (!(atomicOr(reinterpret_cast<unsigned*>(p.work) + 4 + (cand >> 5), bit) & bit)) v = cand;
-    }
-    __threadfence();
-    atomicAdd(p.work + 1, 1);
-    if (v < 0) {
-      int k = atomicAdd(p.work + 2, 1);
-      while (*reinterpret_cast<volatile int*>(p.work + 1) < (int)gridDim.x) __nanosleep(256);
-      __threadfence();
-      for (int wd = 0; v < 0; ++wd) {
-        const unsigned taken = *reinterpret_cast<volatile unsigned*>(p.work + 4 + wd);
-        for (int bit = 0; bit < 32 && v < 0; ++bit) {
-          const int cand = 32 * wd + bit;
-          if (cand < (int)gridDim.x && !((taken >> bit) & 1u) && k-- == 0) v = cand;
-        }
-      }
-    }
-    *vslot = v;
-  }
 
   // ---- balanced decomposition: prefix of pages per sequence (warp 0), then this warp's range
+  int* pre = reinterpret_cast<int*>(smem + (size_t)kWarps * S * (page_bytes + 8));
   if (warp == 0) {
     int run = 0;
     for (int b0 = 0; b0 < p.batch; b0 += 32) {
@@ -275,11 +236,12 @@ attend_partial_mma(AttnParams p, int S) {
   __syncthreads();
   Decomp dc;
   dc.pre = pre; dc.B = p.batch;
-  dc.rm = make_range_map(p, pre[p.batch]);
-  const int gw = *vslot * kWarps + warp;
+  dc.T = pre[p.batch];
+  dc.W = min((int64_t)(p.n_warps / p.hkv), max((int64_t)1, dc.T / p.pmin));
+  const int gw = blockIdx.x * kWarps + warp;
   const int rng = gw / p.hkv, my_h = gw - rng * p.hkv;
-  const int64_t lo = rng < dc.rm.W ? dc.rm.boundary(rng) : dc.rm.T;
-  const int64_t hi = rng < dc.rm.W ? dc.rm.boundary(rng + 1) : dc.rm.T;
+  const int64_t lo = rng < dc.W ? (int64_t)rng * dc.T / dc.W : dc.T;
+  const int64_t hi = rng < dc.W ? (int64_t)(rng + 1) * dc.T / dc.W : dc.T;
   const int64_t nstream = hi - lo;
   // loader: page indices of stream positions [wb, wb + 32) in window c, [wb + 32, wb + 64) in
   // window n, one per lane; the next window is loaded 32 pages ahead of its use
@@ -315,6 +277,11 @@ attend_partial_mma(AttnParams p, int S) {
     ++inflight;
     return true;
   };
+  if (lane == 0) tl_mark(p.tl, 1, gw, 0);
+  // the first pages depend only on the caller's inputs: start streaming before the prologue ends
+  while (inflight < S && issue_one()) {}
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  if (lane == 0) tl_mark(p.tl, 1, gw, 1);
   while (inflight < S && issue_one()) {}
 
   const int hh = gid % GQ;                    // every tile of this lane serves head hh
@@ -886,16 +853,13 @@ attend_partial_mma(AttnParams p, int S) {
       p.ws_l[row] = l_run;
     }
   }
-  if (lane == 0) tl_mark(p.tl, 1, blockIdx.x * kWarps + warp, 2);
-  // (the merge kernel launches once every CTA has got here: triggering earlier lets its CTAs
-  // take SMs during this grid's tail, and their pre-wait work slowed the last warps — measured
-  // 96 vs 94 µs per C2 decode step)
+  if (lane == 0) tl_mark(p.tl, 1, gw, 2);
 #ifdef OSCAR_PROBE_TL
   if (lane == 0 && p.tl) {
     unsigned smid, wid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
     asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
-    p.tl[(size_t)32768 + (size_t)(blockIdx.x * kWarps + warp) * 4 + 3] = smid | (wid << 16) | ((unsigned long long)gw << 32);
+    p.tl[(size_t)32768 + (size_t)gw * 4 + 3] = smid | (wid << 16) | ((unsigned long long)gw << 32);
   }
 #endif
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");   // let the merge kernel launch
@@ -946,8 +910,6 @@ int stages_for(int page_bytes) {
 }
 }  // namespace
 
-int attend_mma_cta_warps() { return kWarps; }
-
 bool attend_mma_tq(const oscar_ctx& c) { return OSCAR_TQ && c.bits == 2 && pick_tq(c.g, c.ng) != nullptr; }
 
 bool attend_mma_supported(const oscar_ctx& c) {
@@ -957,7 +919,7 @@ bool attend_mma_supported(const oscar_ctx& c) {
 // dynamic smem of the partial kernel: per-warp page rings + their mbarriers + the CTA's page
 // prefix pre[B + 1] (balanced decomposition)
 static int mma_smem(int page_bytes, int B) {
-  return kWarps * stages_for(page_bytes) * (page_bytes + 8) + ((B + 2) * 4 + 15) / 16 * 16;
+  return kWarps * stages_for(page_bytes) * (page_bytes + 8) + ((B + 1) * 4 + 15) / 16 * 16;
 }
 
 // Warps of the persistent grid: SMs x resident CTAs per SM x 4 (every CTA resident at once)

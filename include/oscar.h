@@ -131,10 +131,13 @@ OSCAR_API oscar_status oscar_calib_finalize(const oscar_ctx* ctx, const double* 
  * R_K, R_V: fp32 [H_kv][d][d]; acc: fp64 [H_kv][2][d][d] (C_Q, C_S sums of calib_accumulate;
  * the normalization does not change the argmin); grid: host float[n_grid], values in (0, 1],
  * 1 <= n_grid <= 16; obj: device fp64 [H_kv][2][n_grid] (overwritten).  The per-layer choice is
- * argmin_g Σ_h obj[h][side][g] (binding: Oscar.calib_clip).  N = 0 -> obj = 0. */
+ * argmin_g Σ_h obj[h][side][g] (the sum in head order, ties to the earlier grid entry),
+ * written by the library to choice: device int32 [2] = (index for rho_K, index for rho_V), or
+ * NULL to skip the selection.  N = 0 -> obj = 0 (and choice = (0, 0)). */
 OSCAR_API oscar_status oscar_calib_clip(const oscar_ctx* ctx, const void* K, const void* V, int64_t N,
                               const float* R_K, const float* R_V, const double* acc,
-                              const float* grid, int32_t n_grid, double* obj, void* stream);
+                              const float* grid, int32_t n_grid, double* obj, int32_t* choice,
+                              void* stream);
 
 /* ---------------------------------------------------------------- quantize_append(K, V)
  * For each of the T rows and each KV head h: x̃ = x·R_h (K with R_K, V with R_V), per-token

@@ -60,7 +60,7 @@ _sig = {
     "oscar_set_variant": (_i32, [_vp, _i32]),
     "oscar_calib_sv": (_i32, [_vp, _vp, _vp, _vp, _vp, _i32, _i64, _vp, _vp]),
     "oscar_calib_clip": (_i32, [_vp, _vp, _vp, _i64, _vp, _vp, _vp, ctypes.POINTER(ctypes.c_float), _i32, _vp,
-                                _vp]),
+                                _vp, _vp]),
 }
 for _name, (_res, _args) in _sig.items():
     _f = getattr(_lib, _name)
@@ -152,17 +152,18 @@ class Oscar:
 
     def calib_clip(self, K, V, R_K, R_V, acc, grid, obj=None, stream=None):
         """CalibrateClip (reading Z34): surrogate objectives obj [H_kv, 2, n_grid] (fp64, device)
-        and the per-layer choice (rho_K, rho_V) = argmin over the grid of the sum over KV heads
-        (first grid entry on ties).  Synchronizes to read the objectives back."""
+        and the per-layer choice (rho_K, rho_V) the library selects (argmin over the grid of the
+        sum over KV heads, first grid entry on ties).  Synchronizes to read the two indices."""
         import torch
         n = len(grid)
         if obj is None:
             obj = torch.empty((self.cfg.num_kv_heads, 2, n), dtype=torch.float64, device=K.device)
+        choice = torch.empty(2, dtype=torch.int32, device=K.device)
         g = (ctypes.c_float * n)(*[float(x) for x in grid])
         _check(_lib.oscar_calib_clip(self._h, _ptr(K), _ptr(V), K.shape[0], _ptr(R_K), _ptr(R_V), _ptr(acc),
-                                     g, n, _ptr(obj), _stream(stream)), "oscar_calib_clip")
-        tot = obj.sum(dim=0).cpu()
-        return obj, float(grid[int(torch.argmin(tot[0]))]), float(grid[int(torch.argmin(tot[1]))])
+                                     g, n, _ptr(obj), _ptr(choice), _stream(stream)), "oscar_calib_clip")
+        ik, iv = choice.tolist()
+        return obj, float(grid[ik]), float(grid[iv])
 
     # ---------------------------------------------------------------- quantize_append
     def quantize_append(self, K, V, slots, R_K, R_V, pool, stream=None):

@@ -171,7 +171,8 @@ oscar_status oscar_calib_sv(const oscar_ctx* ctx, const void* Q, const void* K, 
 
 oscar_status oscar_calib_clip(const oscar_ctx* ctx, const void* K, const void* V, int64_t N,
                               const float* R_K, const float* R_V, const double* acc,
-                              const float* grid, int32_t n_grid, double* obj, void* stream) {
+                              const float* grid, int32_t n_grid, double* obj, int32_t* choice,
+                              void* stream) {
   if (!ctx) return fail(OSCAR_ERR_ARG, "NULL ctx");
   if (N < 0) return fail(OSCAR_ERR_ARG, "N must be >= 0 (got %lld)", (long long)N);
   if (!grid || n_grid < 1 || n_grid > oscar::kMaxClipGrid)
@@ -183,10 +184,15 @@ oscar_status oscar_calib_clip(const oscar_ctx* ctx, const void* K, const void* V
     kidx[g] = (int32_t)std::ceil((double)grid[g] * ctx->d) - 1;     // reading Z6 nearest rank
   }
   cudaStream_t s = as_stream(stream);
-  if (N == 0)
-    return cuda_status(cudaMemsetAsync(obj, 0, sizeof(double) * ctx->hkv * 2 * n_grid, s), "calib_clip");
-  if (!K || !V || !R_K || !R_V || !acc) return fail(OSCAR_ERR_ARG, "oscar_calib_clip: NULL pointer");
-  return cuda_status(oscar::launch_calib_clip(*ctx, K, V, N, R_K, R_V, acc, kidx, n_grid, obj, s), "calib_clip");
+  oscar_status st;
+  if (N == 0) {
+    st = cuda_status(cudaMemsetAsync(obj, 0, sizeof(double) * ctx->hkv * 2 * n_grid, s), "calib_clip");
+  } else {
+    if (!K || !V || !R_K || !R_V || !acc) return fail(OSCAR_ERR_ARG, "oscar_calib_clip: NULL pointer");
+    st = cuda_status(oscar::launch_calib_clip(*ctx, K, V, N, R_K, R_V, acc, kidx, n_grid, obj, s), "calib_clip");
+  }
+  if (st != OSCAR_OK || !choice) return st;
+  return cuda_status(oscar::launch_clip_select(*ctx, obj, n_grid, choice, s), "calib_clip select");
 }
 
 oscar_status oscar_calib_finalize(const oscar_ctx* ctx, const double* acc, int32_t n_mats,

@@ -86,19 +86,26 @@ cudaError_t launch_cov_accum(const oscar_ctx& c, const void* Q, const void* SV, 
 }
 
 // ------------------------------------------------------------------------------------
-// jacobi_compose: grid (n_mats * 2), 512 threads, ~194 KB dynamic smem.
+// jacobi_compose: grid (n_mats * 2), 512 threads, ~199 KB dynamic smem.
 // Round-robin (circle) ordering: 127 rounds of 64 disjoint (p, q) pairs per sweep.
 // Rotation per Golub & Van Loan sym.schur2: tau = (a_qq - a_pp) / (2 a_pq),
 // t = sign(tau) / (|tau| + sqrt(1 + tau^2)), c = 1/sqrt(1 + t^2), s = t c;
 // A <- Jᵀ A J (rows then columns), V <- V J.
+// Layout: A (fp64) and V (fp32) rows padded to kLd = 129 elements, and one WARP per pair in both
+// passes: the row pass reads A[p][j], A[q][j] with lane = j (consecutive), the column pass
+// A[i][p], A[i][q] and V[i][p], V[i][q] with lane = i (stride 129: distinct banks) — the
+// previous 8-threads-per-pair mapping strided 128 B / 16 rows across lanes (8-16-way bank
+// conflicts, ~19 µs per round).  The column pass also zeroes the annihilated A[p][q], A[q][p].
 // ------------------------------------------------------------------------------------
 constexpr int kJacThreads = 512;
+constexpr int kJacWarps = kJacThreads / 32;
 constexpr int kMaxSweeps = 100;
 constexpr double kJacTol = 1e-12;   // max |offdiag| <= kJacTol * ||A||_F
+constexpr int kLd = kD + 1;
 
 struct JacSmem {
-  double A[kD][kD];
-  float V[kD][kD];
+  double A[kD][kLd];
+  float V[kD][kLd];
   double cs[kD / 2], sn[kD / 2];
   int pp[kD / 2], qq[kD / 2];
   double red[kJacThreads / 32];
@@ -132,7 +139,7 @@ jacobi_compose_kernel(const double* __restrict__ acc, double inv_rows, float* __
   extern __shared__ __align__(16) unsigned char smem_raw[];
   JacSmem& S = *reinterpret_cast<JacSmem*>(smem_raw);
   const int mat = blockIdx.x >> 1, which = blockIdx.x & 1;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const double* src = acc + (size_t)blockIdx.x * kD * kD;   // [n_mats][2][d][d]
 
   double fro2 = 0.0;
@@ -171,34 +178,34 @@ jacobi_compose_kernel(const double* __restrict__ acc, double inv_rows, float* __
         S.cs[tid] = c; S.sn[tid] = s; S.pp[tid] = p; S.qq[tid] = q;
       }
       __syncthreads();
-      {  // rows: (JᵀA)_p = c A_p - s A_q ; (JᵀA)_q = s A_p + c A_q
-        const int k = tid >> 3, j0 = (tid & 7) * 16;
+      // rows: (JᵀA)_p = c A_p - s A_q ; (JᵀA)_q = s A_p + c A_q   (warp per pair, lane = column)
+      for (int k = warp; k < kD / 2; k += kJacWarps) {
         const int p = S.pp[k], q = S.qq[k];
         const double c = S.cs[k], s = S.sn[k];
-#pragma unroll 4
-        for (int j = j0; j < j0 + 16; ++j) {
+#pragma unroll
+        for (int m = 0; m < kD / 32; ++m) {
+          const int j = lane + 32 * m;
           const double ap = S.A[p][j], aq = S.A[q][j];
           S.A[p][j] = c * ap - s * aq;
           S.A[q][j] = s * ap + c * aq;
         }
       }
       __syncthreads();
-      {  // columns of A and of V
-        const int k = tid >> 3, i0 = (tid & 7) * 16;
+      // columns of A and of V (warp per pair, lane = row); the annihilated pair set to 0
+      for (int k = warp; k < kD / 2; k += kJacWarps) {
         const int p = S.pp[k], q = S.qq[k];
         const double c = S.cs[k], s = S.sn[k];
-#pragma unroll 4
-        for (int i = i0; i < i0 + 16; ++i) {
+#pragma unroll
+        for (int m = 0; m < kD / 32; ++m) {
+          const int i = lane + 32 * m;
           const double ap = S.A[i][p], aq = S.A[i][q];
-          S.A[i][p] = c * ap - s * aq;
-          S.A[i][q] = s * ap + c * aq;
+          S.A[i][p] = (i == q) ? 0.0 : c * ap - s * aq;
+          S.A[i][q] = (i == p) ? 0.0 : s * ap + c * aq;
           const double vp = S.V[i][p], vq = S.V[i][q];
           S.V[i][p] = (float)(c * vp - s * vq);
           S.V[i][q] = (float)(s * vp + c * vq);
         }
       }
-      __syncthreads();
-      if (tid < kD / 2) { S.A[S.pp[tid]][S.qq[tid]] = 0.0; S.A[S.qq[tid]][S.pp[tid]] = 0.0; }
       __syncthreads();
     }
   }
@@ -229,7 +236,6 @@ jacobi_compose_kernel(const double* __restrict__ acc, double inv_rows, float* __
   __syncthreads();
   // ---- R = U · H_Had · P_br: per row, FWHT (Sylvester order) then out[beta(e)] = y[e]
   float* R = (which == 0 ? RK : RV) + (size_t)mat * kD * kD;
-  const int warp = tid >> 5, lane = tid & 31;
   const double norm = 0.08838834764831845;   // 1/sqrt(128)
   for (int r = warp; r < kD; r += kJacThreads / 32) {
     double y[4];

@@ -140,4 +140,27 @@ cudaError_t launch_calib_clip(const oscar_ctx& c, const void* K, const void* V, 
   return cudaGetLastError();
 }
 
+// CalibrateClip selection (Alg. 1 P:L1609 "c_K, c_V <- CalibrateClip", reading Z34; S:L190 one
+// pair per layer): thread `side` sums its objective over the KV heads in head order (fp64) for
+// every grid entry and keeps the first minimum.
+__global__ void clip_select_kernel(const double* __restrict__ obj, int hkv, int n_grid,
+                                   int32_t* __restrict__ choice) {
+  const int side = threadIdx.x;
+  if (side >= 2) return;
+  int best = 0;
+  double bv = 0.0;
+  for (int g = 0; g < n_grid; ++g) {
+    double tot = 0.0;
+    for (int h = 0; h < hkv; ++h) tot += obj[((size_t)h * 2 + side) * n_grid + g];
+    if (g == 0 || tot < bv) { bv = tot; best = g; }
+  }
+  choice[side] = best;
+}
+
+cudaError_t launch_clip_select(const oscar_ctx& c, const double* obj, int n_grid, int32_t* choice,
+                               cudaStream_t s) {
+  clip_select_kernel<<<1, 32, 0, s>>>(obj, c.hkv, n_grid, choice);
+  return cudaGetLastError();
+}
+
 }  // namespace oscar

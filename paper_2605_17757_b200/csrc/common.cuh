@@ -36,6 +36,9 @@ constexpr int kMaxClipGrid = 16;
 cudaError_t launch_calib_clip(const oscar_ctx& c, const void* K, const void* V, int64_t N,
                               const float* RK, const float* RV, const double* acc,
                               const int32_t* kidx, int n_grid, double* obj, cudaStream_t s);
+// CalibrateClip selection (reading Z34): choice[side] = argmin_g Σ_h obj[h][side][g]
+cudaError_t launch_clip_select(const oscar_ctx& c, const double* obj, int n_grid, int32_t* choice,
+                               cudaStream_t s);
 cudaError_t launch_jacobi_compose(const oscar_ctx& c, const double* acc, int n_mats,
                                   double inv_rows, float* RK, float* RV, double* evals,
                                   int32_t* info, cudaStream_t s);

@@ -36,6 +36,13 @@ def test_calib_clip_parity(bits, G, N):
     obj, grk, grv = o.calib_clip(T(K, torch.bfloat16), T(V, torch.bfloat16), T(RK), T(RV), T(acc), GRID)
     got = obj.cpu().numpy()
     assert np.all(np.abs(got - ref) <= 1e-3 * np.abs(ref)), np.abs(got - ref).max()
+    # the library's selection (oscar_calib_clip `choice`): first argmin of the head-summed
+    # objectives it returned (ties to the earlier grid entry)
+    for side, g_pick in enumerate([grk, grv]):
+        tot = got[0, side].copy()
+        for h in range(1, H):
+            tot = tot + got[h, side]
+        assert g_pick == GRID[int(np.argmin(tot))]
     for side, (g_pick, o_pick) in enumerate([(grk, rk), (grv, rv)]):
         tot = np.sort(ref.sum(axis=0)[side])
         if tot[1] - tot[0] > 1e-2 * tot[0]:      # a clear minimum must be found by both

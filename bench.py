@@ -124,13 +124,18 @@ def ncu_traffic(kernels):
         return None
 
 
+def oracle_timed(fn):
+    """Run an oracle call on ONE host thread (BLAS pinned to 1 thread: the oracle's per-token
+    loops are single-threaded anyway, so the core count reported is the one used)."""
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(1):
+        t0 = time.perf_counter()
+        r = fn()
+        return r, time.perf_counter() - t0
+
+
 def cpu_threads():
-    try:
-        from threadpoolctl import threadpool_info
-        n = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
-        return int(n)
-    except Exception:
-        return 1
+    return 1
 
 
 # ------------------------------------------------------------------ reference (CPU oracle) arm
@@ -149,12 +154,14 @@ def run_reference(args, rank):
     q = synth.gen_decode_q(rng, 1, HQ // HKV, D)
     pt = np.arange(max_pages, dtype=np.int32)[None]
     unit_bytes = L_ * TOKHEAD_BYTES + 2 * (HQ // HKV) * D * 2
-    for _ in range(args.warmup):
-        O.attend(q, pt, [L_], pool, RK, RV, fmt, 1)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        O.attend(q, pt, [L_], pool, RK, RV, fmt, 1)
-    dt = time.perf_counter() - t0
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(1):
+        for _ in range(args.warmup):
+            O.attend(q, pt, [L_], pool, RK, RV, fmt, 1)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            O.attend(q, pt, [L_], pool, RK, RV, fmt, 1)
+        dt = time.perf_counter() - t0
     gbs = unit_bytes * args.steps / dt / 1e9
     line = {
         "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": args.gpus,
@@ -187,9 +194,10 @@ def c4_leg(args, world, rank, dev, gen, RK_all, RV_all, hbm_peak, peak_kind):
     import torch
     from paper_2605_17757_b200 import binding as Bnd
     from paper_2605_17757_b200 import synth
-    from paper_2605_17757_b200.parallel import barrier, max_over_ranks
-    hkv = max(1, C4_HKV // world)
-    hq = hkv * (C4_HQ // C4_HKV)
+    from paper_2605_17757_b200.parallel import barrier, kv_head_shard, max_over_ranks
+    kv_lo, kv_hi, q_lo, q_hi = kv_head_shard(C4_HKV, C4_HQ, rank, world) if C4_HKV % world == 0 else \
+        (0, max(1, C4_HKV // world), 0, max(1, C4_HKV // world) * (C4_HQ // C4_HKV))
+    hkv, hq = kv_hi - kv_lo, q_hi - q_lo
     o = Bnd.Oscar(Bnd.Config(num_q_heads=hq, num_kv_heads=hkv, bits=BITS, group_size=G, page_size=P))
     o.set_variant(args.variant)
     max_pages = C4_L // P
@@ -197,8 +205,9 @@ def c4_leg(args, world, rank, dev, gen, RK_all, RV_all, hbm_peak, peak_kind):
              for _ in range(C4_LAYERS)]
     pt = torch.arange(C4_B * max_pages, dtype=torch.int32, device=dev)
     pt = pt[torch.randperm(C4_B * max_pages, generator=gen, device=dev)].reshape(C4_B, max_pages).contiguous()
-    RK = [RK_all[l % RK_all.shape[0], :hkv].contiguous() for l in range(C4_LAYERS)]
-    RV = [RV_all[l % RV_all.shape[0], :hkv].contiguous() for l in range(C4_LAYERS)]
+    # this rank's KV heads [kv_lo, kv_hi) and their rotations (parallel.kv_head_shard)
+    RK = [RK_all[l % RK_all.shape[0], kv_lo:kv_hi].contiguous() for l in range(C4_LAYERS)]
+    RV = [RV_all[l % RV_all.shape[0], kv_lo:kv_hi].contiguous() for l in range(C4_LAYERS)]
     chunk = 4 * 8192                       # prefill in 32k-token slabs (bounded staging memory)
     for l in range(C4_LAYERS):
         for c0 in range(0, C4_B * C4_L, chunk):
@@ -224,21 +233,43 @@ def c4_leg(args, world, rank, dev, gen, RK_all, RV_all, hbm_peak, peak_kind):
     b_.record(); torch.cuda.synchronize()
     ms = max_over_ranks(a.elapsed_time(b_), world) / (reps * C4_LAYERS)
     rank_bytes = C4_B * C4_L * hkv * TOKHEAD_BYTES + 2 * C4_B * hq * D * 2
+    cpu = None
+    if rank == 0 and world == 1 and not getattr(args, "no_cpu", False):
+        # oracle: 1 sequence x 1 KV head (its 8 query heads) x 131072 tokens of layer 0
+        import numpy as np
+        import oracle as O
+        fmt = O.PageFormat(D, BITS, G, P)
+        sub = pools[0][pt[0].long(), :1].cpu().numpy()
+        qn = qs[0][0:1, :C4_HQ // C4_HKV].float().cpu().numpy()
+        (ref, _), dt = oracle_timed(lambda: O.attend(qn, np.arange(max_pages, dtype=np.int32)[None], [C4_L], sub,
+                                                     RK[0][:1].cpu().numpy(), RV[0][:1].cpu().numpy(), fmt, 1))
+        unit_bytes = C4_L * TOKHEAD_BYTES + 2 * (C4_HQ // C4_HKV) * D * 2
+        cpu = {"value": unit_bytes / dt / 1e9, "unit": "GB/s", "cores": cpu_threads(), "kind": "oracle",
+               "sample": "layer 0, sequence 0, kv head 0 (8 q heads) x 131072 tokens (1/128 of a layer-step)",
+               "seconds": dt}
     del pools
-    return {"config": f"C4: B={C4_B}, L={C4_L}, H_q/H_kv = {C4_HQ}/{C4_HKV} (g=8), b={BITS}, G={G}; "
-                      f"{hkv} kv heads per rank x {world} rank(s); {C4_LAYERS} layer pools in turn",
-            "attend_us": ms * 1e3, "GBps_per_rank": rank_bytes / ms / 1e6,
-            "GBps_aggregate": rank_bytes * world / ms / 1e6,
-            "roofline": {"bound": "hbm", "achieved": rank_bytes / ms / 1e6, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": rank_bytes / ms / 1e6 / hbm_peak, "traffic": None,
-                         "kernel": "oscar_attend (prologue+partial+merge), g = 8",
-                         "algorithmic_bytes_per_launch": rank_bytes, "peak_kind": peak_kind}}
+    r = {"config": f"C4: B={C4_B}, L={C4_L}, H_q/H_kv = {C4_HQ}/{C4_HKV} (g=8), b={BITS}, G={G}; "
+                   f"kv heads [{kv_lo}, {kv_hi}) on rank {rank} of {world} (parallel.kv_head_shard); "
+                   f"{C4_LAYERS} layer pools in turn",
+         "attend_us": ms * 1e3, "GBps_per_rank": rank_bytes / ms / 1e6,
+         "GBps_aggregate": rank_bytes * world / ms / 1e6,
+         "roofline": {"bound": "hbm", "achieved": rank_bytes / ms / 1e6, "peak": hbm_peak, "unit": "GB/s",
+                      "frac": rank_bytes / ms / 1e6 / hbm_peak,
+                      "traffic": ncu_traffic(["attend_prologue_kernel<8>", "attend_partial_mma<2, 8, 2, 1>",
+                                              "attend_merge_kernel<8>"]),
+                      "traffic_source": "profiles/ncu_traffic.json (ncu --set full of the C4 launch, per launch)",
+                      "kernel": "oscar_attend (prologue+partial+merge), g = 8",
+                      "algorithmic_bytes_per_launch": rank_bytes, "peak_kind": peak_kind}}
+    if cpu:
+        r["cpu_baseline"] = cpu
+    return r
 
 
-def c5_leg(args, dev, hbm_peak):
+def c5_leg(args, dev, hbm_peak, subset=False):
     """b in {2,3,4} x G in {32,64,128} x B in {1,16,64,256} decode at L = 32768
     (Llama-3-8B shape, random packed pools of the page FORMAT), and prefill-append of 4096 tokens
-    per sequence for B in {1, 16, 64}.  Median of 7 calls after 2 warm-up calls."""
+    per sequence for B in {1, 16, 64}.  Median of 7 calls after 2 warm-up calls.  subset=True (the
+    default bench run): G = 64, B in {1, 16}, every b — the full sweep is `--c5-only`."""
     import torch
     from paper_2605_17757_b200 import binding as Bnd
     from paper_2605_17757_b200 import synth
@@ -256,11 +287,11 @@ def c5_leg(args, dev, hbm_peak):
 
     RK, RV = synth.torch_rotation(gen, HKV, D, dev), synth.torch_rotation(gen, HKV, D, dev)
     for bits in (2, 3, 4):
-        for g in (32, 64, 128):
+        for g in ((64,) if subset else (32, 64, 128)):
             o = Bnd.Oscar(Bnd.Config(num_q_heads=HQ, num_kv_heads=HKV, bits=bits, group_size=g, page_size=P))
             o.set_variant(args.variant)
             tok_b = 2 * (D * bits // 8 + 4 * (D // g))
-            for B in (1, 16, 64, 256):
+            for B in ((1, 16) if subset else (1, 16, 64, 256)):
                 mp = L // P
                 pool = synth.torch_random_pool(gen, B * mp, HKV, o.page_bytes(), 2 * P * (D * bits // 8),
                                                P * (D // g), dev)
@@ -290,7 +321,76 @@ def c5_leg(args, dev, hbm_peak):
             torch.cuda.synchronize()
     return {"config": "C5 sweep (SURVEY §8(d)): Llama-3-8B shape (32 q / 8 kv heads, d 128), page 64; decode "
                       "attend at L = 32768 over random packed pools; prefill-append 4096 tokens per sequence "
-                      "into randomly placed pages", "peak_GBps": hbm_peak, "points": pts}
+                      "into randomly placed pages" + ("; subset G = 64, B in {1, 16} (full: --c5-only)"
+                                                      if subset else ""), "peak_GBps": hbm_peak, "points": pts}
+
+
+def c1_leg(args, dev):
+    """SURVEY §8(d) C1 end to end (the correctness config, oracle in seconds): one KV head,
+    d = 128, 4-bit codes, G = 32, P = 64.  calibrate on the 256 tokens' queries with causal
+    S·V computed on the device (NEXT-3) -> quantize_append of the 256 K/V rows -> attend for 64
+    queries whose page tables all point at the 4 pages (the page indirection).  The oracle runs
+    the same steps on the host with the GPU's rotations (R is not comparable elementwise,
+    reading Z12) and its own S·V; reported: GPU and oracle times and the fp32-output max-abs."""
+    import numpy as np
+    import torch
+    import oracle as O
+    from paper_2605_17757_b200 import binding as Bnd
+    from paper_2605_17757_b200 import synth
+    rng = np.random.default_rng(7)
+    N, B1 = 256, 64
+    Qn = synth.gen_queries(rng, N, 1, 1, D)
+    Kn = synth.gen_keys(rng, N, 1, D)
+    Vn = synth.gen_values(rng, N, 1, D)
+    qn = synth.gen_decode_q(rng, B1, 1, D)
+    o = Bnd.Oscar(Bnd.Config(num_q_heads=1, num_kv_heads=1, bits=4, group_size=32, page_size=P))
+    o.set_variant(args.variant)
+    fmt = O.PageFormat(D, 4, 32, P)
+    bf = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(dev, torch.bfloat16)
+    Q, K, V, q = bf(Qn), bf(Kn), bf(Vn), bf(qn)
+    pt = torch.arange(4, dtype=torch.int32, device=dev).repeat(B1, 1).contiguous()
+    seq = torch.full((B1,), N, dtype=torch.int32, device=dev)
+    slots = torch.arange(N, dtype=torch.int64, device=dev)
+    SV = torch.empty((N, 1, D), dtype=torch.bfloat16, device=dev)
+    acc = torch.zeros((1, 2, D, D), dtype=torch.float64, device=dev)
+    RK = torch.empty((1, D, D), dtype=torch.float32, device=dev)
+    RV = torch.empty_like(RK)
+    pool = torch.zeros((4, 1, o.page_bytes()), dtype=torch.uint8, device=dev)
+    ws = torch.empty(o.attend_workspace_bytes(B1, 4), dtype=torch.uint8, device=dev)
+    out = torch.empty((B1, 1, D), dtype=torch.float32, device=dev)
+    starts = torch.zeros(1, dtype=torch.int32, device=dev)
+
+    def gpu_path():
+        acc.zero_()
+        o.calib_sv(Q, K, V, starts, SV)
+        o.calib_accumulate(Q, SV, acc)
+        o.calib_finalize(acc, 1, N, RK, RV)
+        o.quantize_append(K, V, slots, RK, RV, pool)
+        o.attend(q, pt, seq, pool, RK, RV, ws, out)
+
+    for _ in range(3):
+        gpu_path()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    gpu_path()
+    b.record()
+    torch.cuda.synchronize()
+    rk, rv = RK.cpu().numpy(), RV.cpu().numpy()
+
+    def oracle_path():
+        sv = O.score_value(Qn, Kn, Vn, [N])
+        accq, accs = O.cov_accumulate(Qn, 1), O.cov_accumulate(sv, 1)
+        O.calibrate_from_sums(accq, accs, N)
+        opool = np.zeros((4, 1, fmt.page_bytes), np.uint8)
+        O.quantize_append(Kn, Vn, np.arange(N), rk, rv, fmt, opool)
+        return O.attend(qn, np.tile(np.arange(4, dtype=np.int32), (B1, 1)), [N] * B1, opool, rk, rv, fmt, 1)[0]
+
+    ref, dt = oracle_timed(oracle_path)
+    return {"config": "C1: 1 kv head, d 128, 4-bit, G 32, P 64; calibrate(256 tokens, causal S·V on device) -> "
+                      "quantize_append(256) -> attend(64 queries over the same 4 pages)",
+            "gpu_ms": a.elapsed_time(b), "oracle_s": dt, "oracle_cores": cpu_threads(),
+            "parity_max_abs_fp32_out": float(np.abs(out.cpu().numpy() - ref).max()), "parity_tolerance": 2e-3}
 
 
 # ------------------------------------------------------------------ GPU arm
@@ -306,6 +406,8 @@ def main():
     ap.add_argument("--no-c4", action="store_true", help="skip the C4 (Llama-3-70B-shaped, 128k) decode leg")
     ap.add_argument("--c4-only", action="store_true", help="run only the C4 decode leg and print its dict")
     ap.add_argument("--c5-only", action="store_true", help="run only the C5 sweep (bits x G x B) and print it")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the oracle (cpu_baseline) legs")
+    ap.add_argument("--no-graph", action="store_true", help="time the step as plain stream launches only")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -321,6 +423,19 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+    elif not args.no_extras:
+        # a 1-rank NCCL group, so the calibration all-reduce (the path's one collective) runs NCCL
+        # at N = 1 too (a no-op sum, but the real code path)
+        try:
+            import socket
+            sk = socket.socket()
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+            sk.close()
+            dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                                    device_id=dev)
+        except Exception as e:   # NCCL unavailable: the all-reduce is skipped at N = 1
+            print(f"bench: 1-rank NCCL group not available ({e})", file=sys.stderr)
     from paper_2605_17757_b200 import binding as Bnd
     from paper_2605_17757_b200 import synth
     from paper_2605_17757_b200.parallel import allreduce_covariances, barrier, max_over_ranks
@@ -393,6 +508,21 @@ def main():
         sv_flops = 2 * 2 * HQ * D * (calib_tokens // 8192) * (8192 * 8193 // 2)
         del Kc, Vc, SVd
         sweeps = info.cpu().numpy()
+        cpu_cal = None
+        if rank == 0 and world == 1 and not args.no_cpu:
+            import oracle as O
+            ns = 16384                           # 1/4 of a layer's shard; extrapolated per token
+            Qh = Q[:ns].float().cpu().numpy()
+            SVh = SV[:ns].float().cpu().numpy()
+            _, t_cov = oracle_timed(lambda: (O.cov_accumulate(Qh, HKV), O.cov_accumulate(SVh, HKV)))
+            acc_h = acc[0].cpu().numpy()
+            _, t_eig = oracle_timed(lambda: O.calibrate_from_sums(acc_h[:, 0], acc_h[:, 1], calib_tokens * (HQ // HKV)))
+            t_all = t_cov * (calib_tokens / ns) * NL + t_eig * (NL * HKV * 2) / 16
+            cpu_cal = {"value": 2 * ns * HQ * D * 2 / t_cov / 1e9, "unit": "GB/s", "cores": cpu_threads(),
+                       "kind": "oracle", "sample": f"cov_accumulate of {ns} tokens x {HQ} q heads (Q and SV) of one "
+                                                   f"layer + 16 eigensolves (8 kv heads x K,V), extrapolated",
+                       "cov_seconds": t_cov, "eig_seconds_16": t_eig,
+                       "extrapolated_seconds_per_rank_shard": t_all}
         cov_bytes = NL * 2 * calib_tokens * HQ * D * 2
         cov_flops = NL * 2 * calib_tokens * HQ * 2 * D * D
         extras["calibration"] = {
@@ -401,6 +531,7 @@ def main():
             "accumulate_ms": t_acc, "accumulate_GBps": cov_bytes / t_acc / 1e6,
             "accumulate_TFLOPs": cov_flops / t_acc / 1e9,
             "allreduce_ms": t_ar, "allreduce_bytes": acc.numel() * 8,
+            "allreduce_backend": (dist.get_backend() if dist.is_initialized() else "none (1 rank)"),
             "finalize_ms": t_fin, "jacobi_sweeps_max": int(sweeps.max()),
             "sv_ms_per_layer": t_sv, "sv_TFLOPs": sv_flops / t_sv / 1e9,
             "sv_config": f"causal S·V, {calib_tokens // 8192} sequences x 8192 tokens, {HQ} q-heads",
@@ -412,6 +543,8 @@ def main():
                          "kernel": "cov_accum_tc_kernel (tcgen05 + TMA), per layer launch",
                          "algorithmic_bytes_per_launch": cov_bytes // NL, "peak_kind": peak_kind},
         }
+        if cpu_cal:
+            extras["calibration"]["cpu_baseline"] = cpu_cal
         del Q, SV, acc
     else:
         for l in range(NL):
@@ -442,6 +575,20 @@ def main():
         t = ea.elapsed_time(eb) / reps
         t = max_over_ranks(t, world)
         ap_bytes = Tpre * HKV * APPEND_BYTES_PER_TOKHEAD
+        cpu_app = None
+        if rank == 0 and world == 1 and not args.no_cpu:
+            import numpy as np
+            import oracle as O
+            na = 8192                            # 1/64 of the prefill, tokens/s scale linearly
+            Kh, Vh = Kp[:na].float().cpu().numpy(), Vp[:na].float().cpu().numpy()
+            rkh, rvh = RK_all[0].cpu().numpy(), RV_all[0].cpu().numpy()
+            fmt_h = O.PageFormat(D, BITS, G, P)
+            pool_h = np.zeros((na // P, HKV, fmt_h.page_bytes), np.uint8)
+            _, t_app = oracle_timed(lambda: O.quantize_append(Kh, Vh, np.arange(na), rkh, rvh, fmt_h, pool_h))
+            cpu_app = {"value": na * HKV * APPEND_BYTES_PER_TOKHEAD / t_app / 1e9, "unit": "GB/s",
+                       "tokens_per_s": na / t_app, "cores": cpu_threads(), "kind": "oracle",
+                       "sample": f"quantize_append of {na} of the {Tpre} prefill tokens (1/64), 8 kv heads",
+                       "seconds": t_app}
         extras["append"] = {
             "config": f"C2 prefill: {Tpre} tokens x {HKV} kv heads into one layer pool (per rank)",
             "tokens_per_s": Tpre * world / t * 1e3, "token_heads_per_s": Tpre * HKV * world / t * 1e3,
@@ -452,6 +599,8 @@ def main():
                          "kernel": "append_tc_kernel (tcgen05 + TMA)",
                          "algorithmic_bytes_per_launch": ap_bytes, "peak_kind": peak_kind},
         }
+        if cpu_app:
+            extras["append"]["cpu_baseline"] = cpu_app
     del Kp, Vp
 
     # ---------------- decode step inputs (per layer)
@@ -478,20 +627,49 @@ def main():
         for l in range(NL):
             layer(l)
     torch.cuda.synchronize()
-    # timed region: K whole steps, events only at its two ends (per-call events would add their
-    # own stream commands to the step)
-    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier(world)
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        t_start.record()
-        for s in range(args.steps):
+    # the step (NL decode_step calls, 3 kernels each, PDL-chained) captured once in a CUDA graph
+    # (SURVEY §8(d) C2); replays launch the 96 kernels without host launch overhead
+    graph, graph_err = None, None
+    if not args.no_graph:
+        try:
+            graph = torch.cuda.CUDAGraph()
+            cap = torch.cuda.Stream()
+            cap.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(cap):
+                with torch.cuda.graph(graph, stream=cap):
+                    for l in range(NL):
+                        layer(l)
+            torch.cuda.current_stream().wait_stream(cap)
+            for _ in range(args.warmup):
+                graph.replay()
+            torch.cuda.synchronize()
+        except Exception as e:                  # capture unsupported: plain stream launches
+            graph, graph_err = None, str(e)
+
+    def step():
+        if graph is not None:
+            graph.replay()
+        else:
             for l in range(NL):
                 layer(l)
+
+    def timed_steps(fn):
+        # timed region: K whole steps, events only at its two ends (per-call events would add
+        # their own stream commands to the step)
+        t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier(world)
+        torch.cuda.synchronize()
+        t_start.record()
+        for _ in range(args.steps):
+            fn()
         t_end.record()
         torch.cuda.synchronize()
-    barrier(world)
-    ms_total = max_over_ranks(t_start.elapsed_time(t_end), world)
+        barrier(world)
+        return max_over_ranks(t_start.elapsed_time(t_end), world)
+
+    with ClockSampler(local) as clk:
+        ms_total = timed_steps(step)
+    ms_stream = ms_total if graph is None else timed_steps(lambda: [layer(l) for l in range(NL)])
     ms_step = ms_total / args.steps
     value = step_bytes * world * args.steps / (ms_total * 1e-3) / 1e9
     # the step is NL decode_step calls and nothing else: the average call duration over the timed
@@ -563,9 +741,10 @@ def main():
     if not args.no_extras and not args.no_c4:
         extras["c4_decode"] = c4_leg(args, world, rank, dev, gen, RK_all, RV_all, hbm_peak, peak_kind)
 
+
     # ---------------- CPU oracle beside the GPU (rank 0, N=1 only, bounded sample)
     cpu = None
-    if rank == 0 and world == 1 and not args.no_extras:
+    if rank == 0 and world == 1 and not args.no_extras and not args.no_cpu:
         import oracle as O
         fmt = O.PageFormat(D, BITS, G, P)
         b = 0
@@ -573,9 +752,7 @@ def main():
         qn = qs[0][b:b + 1].float().cpu().numpy()
         rk, rv = RK_all[0].cpu().numpy(), RV_all[0].cpu().numpy()
         pt_local = np.arange(max_pages, dtype=np.int32)[None]
-        t0 = time.perf_counter()
-        ref, _ = O.attend(qn, pt_local, [L_], sub, rk, rv, fmt, HKV)
-        dt = time.perf_counter() - t0
+        (ref, _), dt = oracle_timed(lambda: O.attend(qn, pt_local, [L_], sub, rk, rv, fmt, HKV))
         samp_bytes = L_ * HKV * TOKHEAD_BYTES + 2 * HQ * D * 2
         out32 = torch.empty((B_, HQ, D), dtype=torch.float32, device=dev)     # fp32-output mode (Z25)
         o.attend(qs[0], page_table, seq_lens, pools[0], RK_all[0], RV_all[0], ws, out32)
@@ -584,6 +761,11 @@ def main():
                "sample": "layer 0, sequence 0, all 8 kv heads x 32768 tokens (1/16 of one layer-step)",
                "seconds": dt, "parity_max_abs_fp32_out": float(np.abs(got - ref[0]).max()),
                "parity_tolerance": 2e-3}
+
+    if not args.no_extras and rank == 0:
+        if not args.no_cpu and world == 1:
+            extras["c1_end_to_end"] = c1_leg(args, dev)
+        extras["c5_subset"] = c5_leg(args, dev, hbm_peak, subset=True)
 
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
@@ -610,6 +792,10 @@ def main():
                         "algorithmic_bytes_per_launch": attn_bytes,
                         "kernel": "oscar_attend (prologue + partial + merge)"},
         "gpu_launches": launches_per_layer * NL * args.steps,
+        "launch_mode": "cuda_graph (one graph of the 32-layer step, replayed)" if graph is not None else
+                       f"stream launches{' (graph capture failed: ' + graph_err + ')' if graph_err else ''}",
+        "stream_launches": {"ms_per_step": ms_stream / args.steps,
+                            "GBps": step_bytes * world * args.steps / (ms_stream * 1e-3) / 1e9},
         "clocks": clk.summary(),
         "variant": args.variant,
     }
@@ -620,7 +806,7 @@ def main():
     line.update(extras)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 

@@ -34,10 +34,10 @@ def batch_shard(batch: int, rank: int, world: int) -> tuple[int, int]:
 def allreduce_covariances(acc, world: int):
     """SUM the unnormalized covariance accumulators of all ranks in place (§3 targets are
     sums over tokens, so shard partials add exactly up to fp64 rounding)."""
-    if world <= 1:
-        return acc
     import torch.distributed as dist
-    dist.all_reduce(acc, op=dist.ReduceOp.SUM)
+    if world <= 1 and not (dist.is_available() and dist.is_initialized()):
+        return acc
+    dist.all_reduce(acc, op=dist.ReduceOp.SUM)       # (a 1-rank group still runs the collective)
     return acc
 
 

@@ -217,6 +217,15 @@ OSCAR_API oscar_status oscar_rotate(const oscar_ctx* ctx, const void* X, const f
                           int64_t T, void* stream);
 OSCAR_API oscar_status oscar_quantize_rotated(const oscar_ctx* ctx, const float* Krot, const float* Vrot,
                                     const int64_t* slots, int64_t T, void* pool, void* stream);
+/* oscar_rotate_fwht: the north star's second rotation form, measured against oscar_rotate
+ * (DESIGN.md §7.2): Xrot = ((X · U[h]) · H_Had) · P_br with U the d×d matrix of sorted, sign-
+ * normalized eigenvectors (R = U·H·P_br, Eq. 3; H Sylvester-ordered and normalized,
+ * App A.1; out[j] = in[β(j)]) — a tcgen05 GEMM with U followed by a
+ * Walsh–Hadamard transform in registers.  X: bf16 [T][H_kv][d], 16-B aligned; U: fp32
+ * [H_kv][d][d]; Xrot: fp32 [T][H_kv][d].  OSCAR_ERR_UNSUPPORTED when the tensor-core append
+ * path does not apply (clipping configured, misaligned rows). */
+OSCAR_API oscar_status oscar_rotate_fwht(const oscar_ctx* ctx, const void* X, const float* U, float* Xrot,
+                               int64_t T, void* stream);
 
 /* Kernel variant selection for measurements: 0 = default (fastest), 1 =
  * the simple CUDA-core reference kernels.  Applies to quantize_append and attend. */

@@ -24,7 +24,8 @@ EXPORTED = [
     "oscar_create", "oscar_destroy", "oscar_last_error", "oscar_version", "oscar_page_bytes",
     "oscar_calib_accumulate", "oscar_calib_finalize", "oscar_quantize_append",
     "oscar_attend_workspace_bytes", "oscar_attend", "oscar_attend_mixed", "oscar_rotate",
-    "oscar_quantize_rotated", "oscar_set_variant", "oscar_calib_clip", "oscar_calib_sv", "oscar_decode_step",
+    "oscar_quantize_rotated", "oscar_rotate_fwht", "oscar_set_variant", "oscar_calib_clip", "oscar_calib_sv",
+    "oscar_decode_step",
 ]
 
 
@@ -56,6 +57,7 @@ _sig = {
     "oscar_attend_mixed": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i32,
                                   _vp, _sz, _vp, _i32, _vp, _vp]),
     "oscar_rotate": (_i32, [_vp, _vp, _vp, _vp, _i64, _vp]),
+    "oscar_rotate_fwht": (_i32, [_vp, _vp, _vp, _vp, _i64, _vp]),
     "oscar_quantize_rotated": (_i32, [_vp, _vp, _vp, _vp, _i64, _vp, _vp]),
     "oscar_set_variant": (_i32, [_vp, _i32]),
     "oscar_calib_sv": (_i32, [_vp, _vp, _vp, _vp, _vp, _i32, _i64, _vp, _vp]),
@@ -206,6 +208,10 @@ class Oscar:
     def rotate(self, X, R, Xrot, stream=None):
         _check(_lib.oscar_rotate(self._h, _ptr(X), _ptr(R), _ptr(Xrot), X.shape[0],
                                  _stream(stream)), "oscar_rotate")
+
+    def rotate_fwht(self, X, U, Xrot, stream=None):
+        _check(_lib.oscar_rotate_fwht(self._h, _ptr(X), _ptr(U), _ptr(Xrot), X.shape[0],
+                                      _stream(stream)), "oscar_rotate_fwht")
 
     def quantize_rotated(self, Krot, Vrot, slots, pool, stream=None):
         _check(_lib.oscar_quantize_rotated(self._h, _ptr(Krot), _ptr(Vrot), _ptr(slots),

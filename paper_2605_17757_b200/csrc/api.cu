@@ -242,6 +242,19 @@ oscar_status oscar_rotate(const oscar_ctx* ctx, const void* X, const float* R, f
                                    as_stream(stream)), "rotate");
 }
 
+oscar_status oscar_rotate_fwht(const oscar_ctx* ctx, const void* X, const float* U, float* Xrot,
+                               int64_t T, void* stream) {
+  if (!ctx) return fail(OSCAR_ERR_ARG, "NULL ctx");
+  if (T < 0) return fail(OSCAR_ERR_ARG, "T must be >= 0");
+  if (T == 0) return OSCAR_OK;
+  if (!X || !U || !Xrot) return fail(OSCAR_ERR_ARG, "oscar_rotate_fwht: NULL pointer");
+  if (!oscar::append_tc_supported(*ctx) || !aligned16(X))
+    return fail(OSCAR_ERR_UNSUPPORTED, "oscar_rotate_fwht: needs the tensor-core append path (no clipping, "
+                                       "16-B aligned rows)");
+  return cuda_status(oscar::launch_append_tc(*ctx, 3, X, X, nullptr, nullptr, nullptr, T, U, U, nullptr, Xrot,
+                                             as_stream(stream)), "rotate_fwht");
+}
+
 oscar_status oscar_quantize_rotated(const oscar_ctx* ctx, const float* Krot, const float* Vrot,
                                     const int64_t* slots, int64_t T, void* pool, void* stream) {
   if (!ctx) return fail(OSCAR_ERR_ARG, "NULL ctx");

@@ -79,6 +79,13 @@ __device__ __forceinline__ constexpr uint32_t magic_words() {
 //        they would quantize as fp32 x̃ (K half only: one "pair" per head).
 // MODE 2 (oscar_quantize_rotated hook): no TMA / MMA; the epilogue warps take the given fp32 x̃
 //        rows in place of the TMEM load and run the identical quantize/pack/store code.
+// MODE 3 (oscar_rotate_fwht): the north star's alternative rotation form, x̃ = ((x·U)·H)·P_br
+//        (Eq. 3, App A.1): the same tcgen05 GEMM with U (the sorted
+//        eigenvectors, hi/lo bf16) in place of R, then per row the Walsh–Hadamard transform in
+//        registers — the stride-64 butterfly first (H_128 = H_2 ⊗ H_64: each thread reads its own
+//        and its partner half's TMEM columns, no exchange), then strides 1..32 over the thread's
+//        64 values — the 1/√128 scale and the bit-reversed column scatter out[j] = z[β(j)].
+//        Written as fp32 rows like MODE 1, so the two rotation forms compare stage for stage.
 template <int BITS, int G, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
 append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant__ CUtensorMap mapV, TcParams p) {
@@ -89,7 +96,7 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
   // still starts after this kernel completes)
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   const int pair = blockIdx.x / p.cpp, sub = blockIdx.x % p.cpp;
-  const int h = MODE == 1 ? pair : pair >> 1, isV = MODE == 1 ? 0 : pair & 1;
+  const int h = (MODE == 1 || MODE == 3) ? pair : pair >> 1, isV = (MODE == 1 || MODE == 3) ? 0 : pair & 1;
   const int ntiles = sub < p.tiles_per_pair ? (p.tiles_per_pair - sub + p.cpp - 1) / p.cpp : 0;
 
   // ---- R -> bf16 hi/lo, transposed to K-major (row n = output channel, k contiguous), SW128
@@ -184,7 +191,7 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
     // slot of this thread's token, loaded one tile ahead (its latency is off the critical path)
     auto load_slot = [&](int i) -> int64_t {
       const int64_t tk = (int64_t)(sub + i * p.cpp) * kTok + r;
-      return (MODE != 1 && i < ntiles && tk < p.T) ? p.slots[tk] : -1;
+      return (MODE != 1 && MODE != 3 && i < ntiles && tk < p.T) ? p.slots[tk] : -1;
     };
     int64_t slot_next = load_slot(par);
     for (int i = par; i < ntiles; i += 2) {
@@ -192,6 +199,48 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
       const int64_t slot = slot_next;
       slot_next = load_slot(i + 2);
       uint32_t v[64];
+      if constexpr (MODE == 3) {
+        // z = x·U·H_128 for this row: stride-64 butterfly from both halves' TMEM columns (32 at a
+        // time), then the 64-point transform of this half in registers
+        mbar_wait(&S.tfull[a], (i >> 1) & 1);
+        fence_after();
+        const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + a * 128;
+        float y[64];
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
+          uint32_t x0[16], x1[16];
+          OSCAR_TMEM_LD16(tbase + 16 * ch, x0);
+          OSCAR_TMEM_LD16(tbase + 64 + 16 * ch, x1);
+          tmem_ld_wait();
+#pragma unroll
+          for (int k = 0; k < 16; ++k)
+            y[16 * ch + k] = half ? __uint_as_float(x0[k]) - __uint_as_float(x1[k])
+                                  : __uint_as_float(x0[k]) + __uint_as_float(x1[k]);
+        }
+        fence_before();
+        // both halves read this accumulator: the arrival count of tempty is one per epilogue warp
+        // of this parity (kEpiWarps / 2), as in the other modes
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.tempty[a]);
+#pragma unroll
+        for (int st = 1; st < 64; st <<= 1)
+#pragma unroll
+          for (int c = 0; c < 64; ++c)
+            if (!(c & st)) {
+              const float u0 = y[c], u1 = y[c + st];
+              y[c] = u0 + u1;
+              y[c + st] = u0 - u1;
+            }
+        const int64_t tk = (int64_t)(sub + i * p.cpp) * kTok + r;
+        if (tk < p.T) {
+          float* dst = p.rot_out + (tk * p.hkv + h) * kD;
+          constexpr float kNorm = 0.08838834764831845f;   // 1/sqrt(128)
+          // out[j] = z[β(j)]: z index 64·half + c lands on column j = β(64·half + c)
+#pragma unroll
+          for (int c = 0; c < 64; ++c) dst[__brev((unsigned)(64 * half + c)) >> 25] = y[c] * kNorm;
+        }
+        continue;
+      }
       if constexpr (MODE != 2) {
         mbar_wait(&S.tfull[a], (i >> 1) & 1);
         fence_after();
@@ -405,7 +454,9 @@ bool append_tc_aligned(const void* K, const void* V) { return aligned16(K) && al
 cudaError_t launch_append_tc(const oscar_ctx& c, int mode, const void* K, const void* V, const float* xin_k,
                              const float* xin_v, const int64_t* slots, int64_t T, const float* RK,
                              const float* RV, void* pool, float* rot_out, cudaStream_t s) {
-  TcFn fn = mode == 0 ? pick<0>(c.bits, c.G) : mode == 1 ? pick<1>(c.bits, c.G) : pick<2>(c.bits, c.G);
+  // (MODE 3 writes only rotated rows: one instance serves every (b, G))
+  TcFn fn = mode == 0 ? pick<0>(c.bits, c.G) : mode == 1 ? pick<1>(c.bits, c.G)
+          : mode == 2 ? pick<2>(c.bits, c.G) : append_tc_kernel<2, 64, 3>;
   if (!fn) return cudaErrorNotSupported;
   CUtensorMap mk{}, mv{};
   if (mode != 2) {
@@ -420,7 +471,7 @@ cudaError_t launch_append_tc(const oscar_ctx& c, int mode, const void* K, const 
   p.lgP = -1;
   for (int k = 0; k < 16; ++k)
     if ((1 << k) == c.P) p.lgP = k;
-  const int pairs = mode == 1 ? c.hkv : 2 * c.hkv;
+  const int pairs = (mode == 1 || mode == 3) ? c.hkv : 2 * c.hkv;
   p.tiles_per_pair = (int)((T + kTok - 1) / kTok);
   int cpp = c.num_sms / pairs;
   if (cpp < 1) cpp = 1;

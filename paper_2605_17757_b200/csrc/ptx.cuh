@@ -104,6 +104,16 @@ __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.
         "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])                                             \
       : "r"(base))
 
+// 16 consecutive fp32 TMEM columns of this thread's lane (32x32b shape, 16 registers)
+#define OSCAR_TMEM_LD16(base, v)                                                                     \
+  asm volatile(                                                                                       \
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, " \
+      "[%16];\n"                                                                                      \
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),           \
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),       \
+        "=r"(v[14]), "=r"(v[15])                                                                       \
+      : "r"(base))
+
 // ---------------------------------------------------------------- host: tensor-map encoder
 // cuTensorMapEncodeTiled through the runtime's driver entry point; resolved once (a function-
 // local static is initialised thread-safely), nullptr if unavailable.

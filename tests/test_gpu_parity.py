@@ -63,6 +63,26 @@ def test_rotate_parity(bits, G, T_, variant):
     assert err.max() <= 1e-5, err.max()
 
 
+@pytest.mark.parametrize("T_", [1, 129, 1000])
+def test_rotate_fwht_parity(T_):
+    """oscar_rotate_fwht (the U-GEMM + Walsh–Hadamard form of the rotation, measured against the
+    dense form in DESIGN.md §7.2): ((x·U)·H)·P_br against the oracle's x·compose_rotation(U),
+    per row <= 1e-5 of ||x̃|| (reading Z26)."""
+    torch = _torch()
+    rng = np.random.default_rng(300 + T_)
+    H = 2
+    X = synth.gen_keys(rng, T_, H, 128)
+    U = np.stack([np.linalg.qr(rng.standard_normal((128, 128)))[0] for _ in range(H)]).astype(np.float32)
+    R = np.stack([O.compose_rotation(U[h].astype(np.float64)) for h in range(H)]).astype(np.float32)
+    o = make(num_q_heads=H, num_kv_heads=H, bits=2, group_size=64)
+    out = torch.full((T_, H, 128), float("nan"), dtype=torch.float32, device="cuda")
+    o.rotate_fwht(T(X, torch.bfloat16), T(U), out)
+    ref = O.rotate(X, R).astype(np.float64)
+    got = out.cpu().numpy().astype(np.float64)
+    err = np.abs(got - ref).max(axis=-1) / np.linalg.norm(ref, axis=-1)
+    assert err.max() <= 1e-5, err.max()
+
+
 # ---------------------------------------------------------------------------- quantizer
 def _adversarial_rows(rng, n, H):
     X = rng.standard_normal((n, H, 128)).astype(np.float32) * rng.uniform(0.01, 30, (n, H, 1)).astype(np.float32)

@@ -237,17 +237,36 @@ def dequantize_rows(codes: np.ndarray, s16: np.ndarray, m16: np.ndarray, G: int)
 
 
 # P:L560 "four 2-bit values packed per byte"; reading Z22: code i of a row occupies bits
-# [b·i, b·i + b) of the row's little-endian bitstream (byte j = bits 8j..8j+7, LSB first).
+# [b·i, b·i + b) of the row's little-endian bitstream (byte j = bits 8j..8j+7, LSB first), for
+# b in {2, 4}.  Reading Z36 (b = 3, a byte-aligned layout so the decode kernel's integer tensor-
+# core operands take the codes in place): the row is two planes — bytes [0, d/4) the 2-bit
+# bitstream of the low bits (code & 3), bytes [d/4, d/4 + d/8) the high bits (code >> 2), the high
+# bit of channel c = 16·j + 4·i + f (0 <= i, f < 4) at byte d/4 + 4·(j // 2) + i, bit 4·(j % 2) + f
+# (d a multiple of 32).  Same bits per row; only their positions differ.
+def _bit_position(i: int, k: int, bits: int, d: int):
+    """(byte, bit) of bit k of code i inside a packed row."""
+    if bits != 3:
+        pos = bits * i + k
+        return pos // 8, pos % 8
+    if k < 2:                                   # low plane: the 2-bit bitstream
+        pos = 2 * i + k
+        return pos // 8, pos % 8
+    j, i4, f = i // 16, (i % 16) // 4, i % 4   # high plane
+    return d // 4 + 4 * (j // 2) + i4, 4 * (j % 2) + f
+
+
 def pack_codes(codes: np.ndarray, bits: int) -> np.ndarray:
     codes = np.asarray(codes, dtype=np.uint8)
     d = codes.shape[-1]
+    if bits == 3 and d % 32:
+        raise ValueError("3-bit rows need d a multiple of 32 (reading Z36)")
     nbytes = d * bits // 8
     out = np.zeros(codes.shape[:-1] + (nbytes,), dtype=np.uint8)
     for i in range(d):
         for k in range(bits):
-            pos = bits * i + k
+            byte, bit_pos = _bit_position(i, k, bits, d)
             bit = (codes[..., i] >> k) & 1
-            out[..., pos // 8] |= (bit << (pos % 8)).astype(np.uint8)
+            out[..., byte] |= (bit << bit_pos).astype(np.uint8)
     return out
 
 
@@ -256,8 +275,8 @@ def unpack_codes(packed: np.ndarray, bits: int, d: int) -> np.ndarray:
     out = np.zeros(packed.shape[:-1] + (d,), dtype=np.uint8)
     for i in range(d):
         for k in range(bits):
-            pos = bits * i + k
-            bit = (packed[..., pos // 8] >> (pos % 8)) & 1
+            byte, bit_pos = _bit_position(i, k, bits, d)
+            bit = (packed[..., byte] >> bit_pos) & 1
             out[..., i] |= (bit << k).astype(np.uint8)
     return out
 
@@ -315,11 +334,21 @@ class PageFormat:
         j = np.arange(rb)
         k = j // 8
         lane = 4 * (j % 8) + (u // 4) % 4
-        if (rb // 8) % 4 == 0:      # b in {2, 4}: words in 16-byte chunks per lane
+        if self.bits != 3:          # b in {2, 4}: words in 16-byte chunks per lane
             word = 128 * (k // 4) + 4 * lane + k % 4
-        else:                       # b = 3: one word per lane
-            word = 32 * k + lane
-        return self.vcodes_off + 16 * rb * (u // 16) + 4 * word + u % 4
+            return self.vcodes_off + 16 * rb * (u // 16) + 4 * word + u % 4
+        # b = 3 (reading Z36): per 16-token tile, the low-plane bytes j < d/4 laid out exactly as
+        # a 2-bit row's bytes (16·d/4 bytes), then the high-plane bytes (16·d/8 bytes): high byte
+        # e = 4·m + i (m = e // 4, i = e % 4) of row u at 16·(4·i + (u // 4) % 4) + 4·m + u % 4
+        # (one 16-byte chunk per (i, 4-token group): the high bits a decode lane needs for its
+        # channels, 4 tokens per 32-bit word)
+        lo = j < self.d // 4
+        word_lo = 128 * (k // 4) + 4 * lane + k % 4
+        off_lo = 4 * word_lo + u % 4
+        e = j - self.d // 4
+        m, i = e // 4, e % 4
+        off_hi = 16 * (self.d // 4) + 16 * (4 * i + (u // 4) % 4) + 4 * m + u % 4
+        return self.vcodes_off + 16 * rb * (u // 16) + np.where(lo, off_lo, off_hi)
 
     def meta_offsets(self, u: int, grp: int):
         """Offsets of the fp16 pairs (s_K, m_K) and (s_V, m_V) of (row u, group grp)."""

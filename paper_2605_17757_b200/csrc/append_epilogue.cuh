@@ -97,12 +97,31 @@ __device__ __forceinline__ void quantize_store_row_warp(const EpiParams& ep, flo
   const int64_t page = slot / ep.P;
   const int off = (int)(slot % ep.P);
   uint8_t* blk = pool + (page * ep.hkv + h) * (int64_t)ep.page_bytes;
+  const int rb = ep.row_bytes;
+  if (ep.bits == 3) {
+    // reading Z36 planes: low-plane byte `lane` = the 2-bit fields of code & 3; the high bits of
+    // this lane's channels 4·lane + f (= 16j + 4i + f with j = lane / 4, i = lane % 4) form the
+    // nibble (lane / 4) % 2 of high byte 4·(lane / 8) + lane % 4, shared with lane ^ 4
+    const uint32_t lo = (uint32_t)(c[0] & 3) | ((uint32_t)(c[1] & 3) << 2) | ((uint32_t)(c[2] & 3) << 4) |
+                        ((uint32_t)(c[3] & 3) << 6);
+    const uint32_t nib = (uint32_t)(c[0] >> 2) | ((uint32_t)(c[1] >> 2) << 1) | ((uint32_t)(c[2] >> 2) << 2) |
+                         ((uint32_t)(c[3] >> 2) << 3);
+    const uint32_t other = __shfl_xor_sync(0xffffffffu, nib, 4);
+    const int jh = 32 + 4 * (lane >> 3) + (lane & 3);
+    const uint8_t hb = (uint8_t)(((lane >> 2) & 1) ? (other | (nib << 4)) : (nib | (other << 4)));
+    if (!isV) {
+      blk[fmt_krow(off) * rb + lane] = (uint8_t)lo;
+      if (!((lane >> 2) & 1)) blk[fmt_krow(off) * rb + jh] = hb;
+    } else {
+      blk[ep.vcodes_off + fmt_vbyte(off, lane, rb)] = (uint8_t)lo;
+      if (!((lane >> 2) & 1)) blk[ep.vcodes_off + fmt_vbyte(off, jh, rb)] = hb;
+    }
+  } else {
   // reading Z22 bitstream: this lane's 4 codes are bits [4·b·lane, 4·b·lane + 4b); byte j of the
-  // row (bits 8j .. 8j+7) lies in the fields of lanes a = 8j/(4b) and a + 1 (b = 3 straddles)
+  // row (bits 8j .. 8j+7) lies in the fields of lanes a = 8j/(4b) and a + 1
   const int fb = 4 * ep.bits;                // bits per lane field
   const uint32_t field = (uint32_t)c[0] | ((uint32_t)c[1] << ep.bits) | ((uint32_t)c[2] << (2 * ep.bits)) |
                          ((uint32_t)c[3] << (3 * ep.bits));
-  const int rb = ep.row_bytes;
 #pragma unroll
   for (int m = 0; m < 2; ++m) {
     const int j = lane + 32 * m;             // byte index inside the row
@@ -115,6 +134,7 @@ __device__ __forceinline__ void quantize_store_row_warp(const EpiParams& ep, flo
       if (!isV) blk[fmt_krow(off) * rb + j] = v;
       else blk[ep.vcodes_off + fmt_vbyte(off, j, rb)] = v;
     }
+  }
   }
   if ((lane % lanes_per_group) == 0) {
     const int grp = lane / lanes_per_group;

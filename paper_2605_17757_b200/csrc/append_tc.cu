@@ -290,21 +290,26 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
       const int u = !valid ? 0 : (p.lgP >= 0 ? (int)(slot & (p.P - 1)) : (int)(slot % p.P));
       uint8_t* blk = p.pool + (page * p.hkv + h) * (int64_t)p.page_bytes;
       // codes: the magic add leaves float bits 0x4B400000 + code; accumulate bits << shift with
-      // one LEA per code and remove the constant part once per word
-      // (3-bit codes straddle words: the code is taken out of the float bits and OR-ed in,
-      // its high bits spilling into the next word)
+      // one LEA per code and remove the constant part once per word.
+      // b = 3 (reading Z36 planes): packed[0..3] = this half's 16 low-plane bytes (the 2-bit
+      // stream of code & 3), packed[4..5] = its 8 high-plane bytes (channel 64·half + idx: high
+      // bit at bit 8·((idx % 16) / 4) + 4·((idx / 16) % 2) + idx % 4 of word idx / 32)
       uint32_t packed[BITS * 2];
 #pragma unroll
       for (int w = 0; w < BITS * 2; ++w) packed[w] = BITS == 3 ? 0u : 0u - magic_words<BITS>();
       auto put = [&](int idx, uint32_t fbits) {
-        const int bit = idx * BITS, wd = bit >> 5, sh = bit & 31;
         if (BITS == 3) {
-          const uint32_t code = fbits - 0x4B400000u;
-          packed[wd] |= code << sh;
-          if (sh > 29) packed[wd + 1] |= code >> (32 - sh);
+          packed[idx >> 4] |= (fbits & 3u) << (2 * (idx & 15));
+          packed[4 + (idx >> 5)] |= ((fbits >> 2) & 1u) << (8 * ((idx & 15) >> 2) + 4 * ((idx >> 4) & 1) + (idx & 3));
         } else {
+          const int bit = idx * BITS, wd = bit >> 5, sh = bit & 31;
           packed[wd] += fbits << sh;
         }
+      };
+      // row byte of this half's packed byte jb (b = 3: low plane 16·half + jb, then high plane)
+      auto row_byte = [&](int jb) -> int {
+        if (BITS == 3) return jb < 16 ? 16 * half + jb : 32 + 8 * half + (jb - 16);
+        return half * (8 * BITS) + jb;
       };
 #pragma unroll
       for (int gi = 0; gi < GPH; ++gi) {
@@ -358,16 +363,16 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
       constexpr int HB = 8 * BITS;                // bytes of this half row
       constexpr int RB = 16 * BITS;               // bytes of a row
       if (!isV) {
-        uint8_t* dst = blk + fmt_krow(u) * p.row_bytes + half * HB;
-        if (HB % 16 == 0) {
+        uint8_t* rowp = blk + fmt_krow(u) * p.row_bytes;
+        if (BITS == 3) {                          // low plane 16 B, high plane 8 B of this half
+          *reinterpret_cast<uint4*>(rowp + 16 * half) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+          *reinterpret_cast<uint2*>(rowp + 32 + 8 * half) = make_uint2(packed[4], packed[5]);
+        } else {
+          uint8_t* dst = rowp + half * HB;
 #pragma unroll
           for (int w4 = 0; w4 < HB / 16; ++w4)
             *reinterpret_cast<uint4*>(dst + 16 * w4) =
                 make_uint4(packed[4 * w4], packed[4 * w4 + 1], packed[4 * w4 + 2], packed[4 * w4 + 3]);
-        } else {                                  // 3-bit: 24-B half rows, 8-B aligned
-#pragma unroll
-          for (int w2 = 0; w2 < HB / 8; ++w2)
-            *reinterpret_cast<uint2*>(dst + 8 * w2) = make_uint2(packed[2 * w2], packed[2 * w2 + 1]);
         }
       } else if (fastV) {
         constexpr int TILE = 16 * RB + 16;        // staged 16-token tile (+16 B: bank shift)
@@ -378,9 +383,11 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
         auto put = [&](auto half_c) {
           constexpr int H = decltype(half_c)::value;
 #pragma unroll
-          for (int jb = 0; jb < HB; ++jb)
-            asm volatile("st.shared.u8 [%0], %1;\n" ::"r"(base + fmt_vbyte(0, H * HB + jb, RB)),
+          for (int jb = 0; jb < HB; ++jb) {
+            const int rbyte = BITS == 3 ? (jb < 16 ? 16 * H + jb : 32 + 8 * H + (jb - 16)) : H * HB + jb;
+            asm volatile("st.shared.u8 [%0], %1;\n" ::"r"(base + fmt_vbyte(0, rbyte, RB)),
                          "r"(packed[jb >> 2] >> (8 * (jb & 3))) : "memory");
+          }
         };
         if (half) put(std::integral_constant<int, 1>{});
         else put(std::integral_constant<int, 0>{});
@@ -408,7 +415,7 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
         uint8_t* vb = blk + p.vcodes_off;
 #pragma unroll
         for (int jb = 0; jb < HB; ++jb)
-          vb[fmt_vbyte(u, half * HB + jb, p.row_bytes)] = (uint8_t)(packed[jb >> 2] >> (8 * (jb & 3)));
+          vb[fmt_vbyte(u, row_byte(jb), p.row_bytes)] = (uint8_t)(packed[jb >> 2] >> (8 * (jb & 3)));
       }
     }
   }

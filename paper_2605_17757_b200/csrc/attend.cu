@@ -257,10 +257,18 @@ __global__ void __launch_bounds__(128) attend_partial_simple(AttnParams p) {
       for (int k = 0; k < nh; ++k) { s[k] = 0.f; dot[k] = 0.f; }
 #pragma unroll
       for (int j = 0; j < kD / 32; ++j) {
-        uint32_t w[BITS + 1];
+        // channels 32j .. 32j+31: b in {2, 4}: the BITS words BITS·j.. of the bitstream; b = 3
+        // (reading Z36): low-plane words 2j, 2j+1 and high-plane word 8 + j (channel
+        // 32j + 4·k4 + r: high bit at bit 8·(k4 % 4) + 4·(k4 / 4) + r)
+        constexpr int NW = BITS == 3 ? 3 : BITS;
+        uint32_t w[NW + 1];
+        if (BITS == 3) {
+          w[0] = kw[2 * j]; w[1] = kw[2 * j + 1]; w[2] = kw[8 + j];
+        } else {
 #pragma unroll
-        for (int u = 0; u < BITS; ++u) w[u] = kw[BITS * j + u];
-        w[BITS] = 0u;
+          for (int u = 0; u < NW; ++u) w[u] = kw[BITS * j + u];
+        }
+        w[NW] = 0u;
 #pragma unroll
         for (int k4 = 0; k4 < 8; ++k4) {
           float4 qv[nh];
@@ -269,8 +277,15 @@ __global__ void __launch_bounds__(128) attend_partial_simple(AttnParams p) {
             qv[k] = reinterpret_cast<const float4*>(qs + (i0 + k * istep) * kD)[8 * j + k4];
 #pragma unroll
           for (int r = 0; r < 4; ++r) {
-            const int bit = BITS * (4 * k4 + r), wi = bit >> 5, sh = bit & 31;
-            const uint32_t v = sh + BITS <= 32 ? (w[wi] >> sh) : __funnelshift_r(w[wi], w[wi + 1], sh);
+            uint32_t v;
+            if (BITS == 3) {
+              const uint32_t lo2 = (w[k4 >> 2] >> (2 * (4 * (k4 & 3) + r))) & 3u;
+              const uint32_t hi1 = (w[2] >> (8 * (k4 & 3) + 4 * (k4 >> 2) + r)) & 1u;
+              v = lo2 | (hi1 << 2);
+            } else {
+              const int bit = BITS * (4 * k4 + r), wi = bit >> 5, sh = bit & 31;
+              v = sh + BITS <= 32 ? (w[wi] >> sh) : __funnelshift_r(w[wi], w[wi + 1], sh);
+            }
             const float cf = (float)(v & ((1u << BITS) - 1u));
 #pragma unroll
             for (int k = 0; k < nh; ++k)
@@ -329,18 +344,24 @@ __global__ void __launch_bounds__(128) attend_partial_simple(AttnParams p) {
     {
       const int c = tid;
       const int grp = c / p.G;
-      const int bit = c * p.bits;
+      // the code's byte(s): b in {2, 4} one byte at bit sh; b = 3 (reading Z36) the low-plane
+      // byte c/4 at bit 2(c%4) and the high-plane byte 32 + 4(j/2) + i (c = 16j + 4i + f) at bit
+      // 4(j%2) + f, gathered by one PRMT as bits 0-7 / 8-15
+      const int bit = BITS == 3 ? 2 * c : c * p.bits;
       const int jb = bit >> 3, sh = bit & 7;
+      const int jh = 32 + 4 * ((c >> 4) >> 1) + ((c >> 2) & 3), shh = 8 + 4 * ((c >> 4) & 1) + (c & 3);
 #pragma unroll
       for (int i = 0; i < g; ++i) acc[i] *= alpha[i];
       for (int t4 = 0; t4 < valid; t4 += 4) {
         const uint32_t w0 = *reinterpret_cast<const uint32_t*>(pg + p.vcodes_off + fmt_vbyte(t4, jb, rb));
-        const uint32_t w1 = sh + BITS > 8
-            ? *reinterpret_cast<const uint32_t*>(pg + p.vcodes_off + fmt_vbyte(t4, jb + 1, rb)) : 0u;
+        const uint32_t w1 = BITS == 3 ? *reinterpret_cast<const uint32_t*>(pg + p.vcodes_off + fmt_vbyte(t4, jh, rb))
+                          : (sh + BITS > 8
+                             ? *reinterpret_cast<const uint32_t*>(pg + p.vcodes_off + fmt_vbyte(t4, jb + 1, rb)) : 0u);
         auto pv_tok = [&](int u) {
           const int t = t4 + u;
           const uint32_t word = __byte_perm(w0, w1, u | ((4 + u) << 4));   // byte u of w0, w1
-          const int code = (int)((word >> sh) & (uint32_t)qmax);
+          const int code = BITS == 3 ? (int)(((word >> sh) & 3u) | (((word >> shh) & 1u) << 2))
+                                     : (int)((word >> sh) & (uint32_t)qmax);
           const float2 sm = vmf[t * p.ng + grp];
           const float v = fmaf(sm.x, (float)code, sm.y);
 #pragma unroll

@@ -174,8 +174,8 @@ struct Decomp {
 template <int BITS, int GQ, int NG, bool TQ>
 __global__ void __launch_bounds__(kWarps * 32, (GQ * NG <= 8 ? OSCAR_MINB : OSCAR_MINB_NT2))
 attend_partial_mma(AttnParams p, int S) {
-  static_assert(!TQ || (BITS == 2 && GQ >= 2 && (NG <= 2 || (NG == 4 && GQ == 4))),
-                "token-row QK layout: 2-bit, g >= 2 (G = 32: g = 4)");
+  static_assert(!TQ || ((BITS == 2 || BITS == 3) && GQ >= 2 && (NG <= 2 || (NG == 4 && GQ == 4))),
+                "token-row QK layout: 2- or 3-bit, g >= 2 (G = 32: g = 4)");
   constexpr int NTQ = (GQ + 3) / 4;           // TQ: QK N-tiles of 4 heads x (hi|lo)
   constexpr int NC = GQ * NG;                 // (group, head) combos
   constexpr int NT = (NC + 7) / 8;            // 8-combo tiles (QK M-tiles / PV N-tiles)
@@ -185,14 +185,18 @@ attend_partial_mma(AttnParams p, int S) {
   // G = 32, g = 4 (PVG too): M-tile pair p takes V words 2p (rows gid: group 2p) / 2p + 1 (rows
   // gid + 8: group 2p + 1); its 8 columns are the 4 heads of group 2p, then of group 2p + 1
   constexpr bool PVG = TQ && ((GQ == 8 && NG == 2) || (GQ == 4 && NG == 4));
+  static_assert(!(PVG && BITS == 3), "3-bit token-row layout: combo-tile PV only");
+  // 3-bit codes (reading Z36): a 2-bit low plane in the 2-bit places plus a 1-bit high plane;
+  // LB = bits of the low plane every in-place operand below is built from
+  constexpr int LB = BITS == 3 ? 2 : BITS;
   constexpr int NTA = PVG ? 1 : NT;           // PV accumulator N-tiles
   constexpr int NBS = PVG ? 2 : NT;           // PV B-operand sets (per M-tile pair, or per N-tile)
   constexpr int kChunk = NT > 1 ? OSCAR_CHUNK_NT2 : OSCAR_CHUNK;   // 16-token sub-tiles per softmax chunk
   constexpr int RB = 16 * BITS;               // packed row bytes (d = 128)
   constexpr int G = 128 / NG;
-  constexpr int CPB = 8 / BITS;
-  constexpr int VW = RB / 8;                  // V words per lane per 16-token tile (4 or 8)
-  constexpr uint32_t kCodeMask = BITS == 2 ? 0x00030003u : 0x000F000Fu;
+  constexpr int CPB = 8 / LB;
+  constexpr int VW = BITS == 3 ? 4 : RB / 8;  // low-plane V words per lane per 16-token tile
+  constexpr uint32_t kCodeMask = LB == 2 ? 0x00030003u : 0x000F000Fu;
   constexpr uint32_t kByteMask = BITS == 2 ? 0x03030303u : 0x0F0F0F0Fu;
   extern __shared__ __align__(128) unsigned char smem[];
 
@@ -594,6 +598,16 @@ attend_partial_mma(AttnParams p, int S) {
                          : "=r"(wa[0]), "=r"(wa[1]), "=r"(wb[0]), "=r"(wb[1])
                          : "r"(addr));
           }
+          // 3-bit: the high-plane words of low words t and 4 + t (high word j / 2, nibble j % 2
+          // = t % 2) of rows gid / gid + 8, normalized so the lane's nibble sits in bits 4-7
+          uint32_t ha[2], hb[2];
+          if constexpr (BITS == 3) {
+            const uint32_t* ra = reinterpret_cast<const uint32_t*>(pg + (size_t)(16 * st + gid) * RB + 32);
+            const uint32_t* rb = reinterpret_cast<const uint32_t*>(pg + (size_t)(16 * st + 8 + gid) * RB + 32);
+            const int sh = (t & 1) ? 0 : 4;
+            ha[0] = ra[t >> 1] << sh; ha[1] = ra[2 + (t >> 1)] << sh;
+            hb[0] = rb[t >> 1] << sh; hb[1] = rb[2 + (t >> 1)] << sh;
+          }
           int cq[NTQ][NG][4];
 #pragma unroll
           for (int jt = 0; jt < NTQ; ++jt)
@@ -611,7 +625,7 @@ attend_partial_mma(AttnParams p, int S) {
               a[1] = (wb[2 * kk] * mul) & 0xC0C0C0C0u;
               a[2] = (wa[2 * kk + 1] * mul) & 0xC0C0C0C0u;
               a[3] = (wb[2 * kk + 1] * mul) & 0xC0C0C0C0u;
-            } else {
+            } else if (BITS == 2) {
               // k-step kk: word kk/2 (group kk/2 when G = 64), 2-bit fields 2(kk&1) (a0, a1) and
               // 2(kk&1)+1 (a2, a3) moved to the top of each byte (c·64, folded into qscale)
               const int wi = kk >> 1, s0 = 6 - 4 * (kk & 1);
@@ -619,10 +633,35 @@ attend_partial_mma(AttnParams p, int S) {
               a[1] = (wb[wi] << s0) & 0xC0C0C0C0u;
               a[2] = (wa[wi] << (s0 - 2)) & 0xC0C0C0C0u;
               a[3] = (wb[wi] << (s0 - 2)) & 0xC0C0C0C0u;
+            } else {
+              // 3-bit: the low field to bits 5-6 (lo·32) — fields f0 = 2(kk&1) and f0 + 1
+              const int wi = kk >> 1;
+              if ((kk & 1) == 0) {
+                a[0] = (wa[wi] << 5) & 0x60606060u;
+                a[1] = (wb[wi] << 5) & 0x60606060u;
+                a[2] = (wa[wi] << 3) & 0x60606060u;
+                a[3] = (wb[wi] << 3) & 0x60606060u;
+              } else {
+                a[0] = (wa[wi] << 1) & 0x60606060u;
+                a[1] = (wb[wi] << 1) & 0x60606060u;
+                a[2] = (wa[wi] >> 1) & 0x60606060u;
+                a[3] = (wb[wi] >> 1) & 0x60606060u;
+              }
             }
             const int g = NG == 4 ? kk : (NG == 2 ? (kk >> 1) : 0);
 #pragma unroll
             for (int jt = 0; jt < NTQ; ++jt) imma16832_us(cq[jt][g], a, bq[jt][kk][0], bq[jt][kk][1]);
+            if constexpr (BITS == 3) {
+              // the high bit to bit 7 (hi·128): code·32 = lo·32 + hi·128 into the same C
+              const int wi = kk >> 1, f0 = 2 * (kk & 1);
+              uint32_t ah[4];
+              ah[0] = (ha[wi] << (3 - f0)) & 0x80808080u;
+              ah[1] = (hb[wi] << (3 - f0)) & 0x80808080u;
+              ah[2] = (ha[wi] << (2 - f0)) & 0x80808080u;
+              ah[3] = (hb[wi] << (2 - f0)) & 0x80808080u;
+#pragma unroll
+              for (int jt = 0; jt < NTQ; ++jt) imma16832_us(cq[jt][g], ah, bq[jt][kk][0], bq[jt][kk][1]);
+            }
           }
           // scores of tokens 2·gid (e = 0) and 2·gid + 1 (e = 1) for head 4·jt + t
 #pragma unroll
@@ -737,13 +776,21 @@ attend_partial_mma(AttnParams p, int S) {
               vw[4 * u] = x.x; vw[4 * u + 1] = x.y; vw[4 * u + 2] = x.z; vw[4 * u + 3] = x.w;
             }
           }
+          // 3-bit: high-plane word k = high byte 4k + gid % 4 of this lane's 4 tokens (FORMAT,
+          // reading Z36); the lane's nibble gid / 4 moved to bits 0-3 of each byte
+          uint32_t vh[BITS == 3 ? 4 : 1];
+          if constexpr (BITS == 3) {
+            const uint4 x = *reinterpret_cast<const uint4*>(vcodes + (size_t)st * 16 * RB + 512 + 16 * (4 * (gid & 3) + t));
+            const int sh = 4 * (gid >> 2);
+            vh[0] = x.x >> sh; vh[1] = x.y >> sh; vh[2] = x.z >> sh; vh[3] = x.w >> sh;
+          }
           uint32_t vs[VW];
 #pragma unroll
           for (int k = 0; k < VW; ++k) vs[k] = vw[k] >> 8;
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int q = i % CPB;
-            const uint32_t msk = kCodeMask << (BITS * q);
+            const uint32_t msk = kCodeMask << (LB * q);
             uint32_t a[4];
             if constexpr (PVG) {               // M-tile i: group p = i / CPB, words 2p / 2p + 1
               const int pg2 = 2 * (i / CPB);
@@ -759,6 +806,18 @@ attend_partial_mma(AttnParams p, int S) {
               a[3] = vs[VW / 2 + i / CPB] & msk;
 #pragma unroll
               for (int j = 0; j < NTA; ++j) hmma16816(acc[i][j], a, bpv[j][0], bpv[j][1]);
+              if constexpr (BITS == 3) {
+                // the high bit at mantissa bit 2q + 2 of each half (4·hi·4^q·2^-24): tokens
+                // (4t, 4t+2) from bytes 0 / 2, (4t+1, 4t+3) from bytes 1 / 3 of word i/4 (+2 upper)
+                const uint32_t mh = 0x00040004u << (2 * q);
+                uint32_t ah[4];
+                ah[0] = (vh[i / CPB] << (q + 2)) & mh;
+                ah[1] = (vh[2 + i / CPB] << (q + 2)) & mh;
+                ah[2] = (vh[i / CPB] >> (6 - q)) & mh;
+                ah[3] = (vh[2 + i / CPB] >> (6 - q)) & mh;
+#pragma unroll
+                for (int j = 0; j < NTA; ++j) hmma16816(acc[i][j], ah, bpv[j][0], bpv[j][1]);
+              }
             }
           }
         }
@@ -815,7 +874,7 @@ attend_partial_mma(AttnParams p, int S) {
         const size_t row = row0 + (size_t)head * p.n_splits;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const float unscale = (float)(1 << (24 - BITS * (i % CPB)));
+          const float unscale = (float)(1 << (24 - LB * (i % CPB)));
           const int ch = 64 * (i / CPB) + CPB * gid + (i % CPB) + (upper ? 32 : 0);
           p.ws_o[row * 128 + ch] = fmaf(acc[i][0][e], unscale, accm[i / CPB][e & 1]);
         }
@@ -831,8 +890,8 @@ attend_partial_mma(AttnParams p, int S) {
                              : __shfl_sync(0xffffffffu, mv_acc[j], 4 * col);   // combo col = gid of lane 4·col
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const float unscale = (float)(1 << (24 - BITS * (i % CPB)));
-          const int ch = pv_channel<BITS>(i, gid, e >> 1);
+          const float unscale = (float)(1 << (24 - LB * (i % CPB)));
+          const int ch = pv_channel<LB>(i, gid, e >> 1);
           if (cc < NC && ch / G == cc / GQ) {
             const size_t row = row0 + (size_t)(cc % GQ) * p.n_splits;
             p.ws_o[row * 128 + ch] = fmaf(acc[i][j % NTA][e], unscale, mvs);
@@ -891,10 +950,20 @@ KernelFn pick_tq(int g, int ng) {
   return nullptr;
 }
 
+// 3-bit (reading Z36 planes) on the token-row layout: the combo-tile PV shapes
+KernelFn pick_tq3(int g, int ng) {
+#define OSCAR_CASE(GQ_, NG_) \
+  if (g == GQ_ && ng == NG_) return attend_partial_mma<3, GQ_, NG_, true>;
+  OSCAR_CASE(2, 1) OSCAR_CASE(2, 2) OSCAR_CASE(4, 1) OSCAR_CASE(4, 2) OSCAR_CASE(8, 1)
+#undef OSCAR_CASE
+  return nullptr;
+}
+
 KernelFn pick(int bits, int g, int ng) {
   if (bits == 2 && OSCAR_TQ) {
     if (KernelFn f = pick_tq(g, ng)) return f;
   }
+  if (bits == 3 && OSCAR_TQ) return pick_tq3(g, ng);
   if (bits == 2) return pick_g<2>(g, ng);
   if (bits == 4) return pick_g<4>(g, ng);
   return nullptr;
@@ -910,7 +979,9 @@ int stages_for(int page_bytes) {
 }
 }  // namespace
 
-bool attend_mma_tq(const oscar_ctx& c) { return OSCAR_TQ && c.bits == 2 && pick_tq(c.g, c.ng) != nullptr; }
+bool attend_mma_tq(const oscar_ctx& c) {
+  return OSCAR_TQ && ((c.bits == 2 && pick_tq(c.g, c.ng) != nullptr) || (c.bits == 3 && pick_tq3(c.g, c.ng) != nullptr));
+}
 
 bool attend_mma_supported(const oscar_ctx& c) {
   return c.d == 128 && pick(c.bits, c.g, c.ng) != nullptr && c.P % 16 == 0 && stages_for(c.page_bytes) > 0;

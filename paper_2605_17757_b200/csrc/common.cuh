@@ -69,9 +69,16 @@ __device__ __forceinline__ float bf16_to_f32(uint16_t b) {
 __host__ __device__ __forceinline__ int fmt_krow(int u) {
   return 16 * (u >> 4) + 8 * (u & 1) + ((u & 15) >> 1);
 }
+// b = 3 (rb = 48, reading Z36: a 2-bit low plane ‖ a 1-bit high plane per row): the 32 low-plane
+// bytes of a 16-token tile take the 2-bit layout (512 B), the 16 high-plane bytes e = 4m + i
+// follow at 512 + 16·(4i + token group) + 4m + token-in-group
 __host__ __device__ __forceinline__ int fmt_vbyte(int u, int j, int rb) {
+  if (rb == 48 && j >= 32) {
+    const int e = j - 32;
+    return 16 * rb * (u >> 4) + 512 + 16 * (4 * (e & 3) + ((u >> 2) & 3)) + 4 * (e >> 2) + (u & 3);
+  }
   const int k = j >> 3, lane = 4 * (j & 7) + ((u >> 2) & 3);
-  const int word = ((rb >> 3) & 3) == 0 ? 128 * (k >> 2) + 4 * lane + (k & 3) : 32 * k + lane;
+  const int word = 128 * (k >> 2) + 4 * lane + (k & 3);
   return 16 * rb * (u >> 4) + 4 * word + (u & 3);
 }
 // offset of the (s_K, m_K) pair; the (s_V, m_V) pair is at +16

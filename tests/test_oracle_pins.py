@@ -326,7 +326,16 @@ def test_residual_monotone_in_bits():
 def test_pack_closed_forms_and_roundtrip():
     assert O.pack_codes(np.array([0, 1, 2, 3], np.uint8), 2).tolist() == [0xE4]
     assert O.pack_codes(np.array([1, 2], np.uint8), 4).tolist() == [0x21]
-    assert O.pack_codes(np.array([1, 2, 3, 4, 5, 6, 7, 0], np.uint8), 3).tolist() == [0xD1, 0x58, 0x1F]
+    # 3-bit (reading Z36, worked by hand): low plane = the 2-bit stream of code & 3, high plane
+    # bit of channel 16j + 4i + f at byte d/4 + 4(j // 2) + i, bit 4(j % 2) + f.  Codes 0..7 four
+    # times: every low byte (0, 1, 2, 3) = 0xE4; the high bit is set exactly for i odd -> bytes
+    # 0x00, 0xFF, 0x00, 0xFF.  A single code 4 on channel 5 (j 0, i 1, f 1) -> byte 9, bit 1.
+    assert O.pack_codes(np.array(list(range(8)) * 4, np.uint8), 3).tolist() == [0xE4] * 8 + [0x00, 0xFF, 0x00, 0xFF]
+    one = np.zeros(32, np.uint8)
+    one[5] = 4
+    assert O.pack_codes(one, 3).tolist() == [0] * 9 + [0x02, 0, 0]
+    with pytest.raises(ValueError):
+        O.pack_codes(np.zeros(8, np.uint8), 3)
     rng = np.random.default_rng(7)
     for bits in [2, 3, 4]:
         c = rng.integers(0, 2 ** bits, size=(20000, 128), dtype=np.uint8)

@@ -25,8 +25,18 @@ namespace oscar {
 
 namespace {
 
+#ifndef OSCAR_TREE_MINMAX
+#define OSCAR_TREE_MINMAX 0      // 1: tree min/max (measured slower: 611 vs 586 us, C2 prefill)
+#endif
 constexpr int kTok = 128;          // tokens per tile (UMMA M)
 constexpr int kStages = 4;
+#ifndef OSCAR_APPEND_L2PF
+#define OSCAR_APPEND_L2PF 0
+#endif
+#ifndef OSCAR_APPEND_ACC
+#define OSCAR_APPEND_ACC 2
+#endif
+constexpr int kAcc = OSCAR_APPEND_ACC;          // TMEM fp32 accumulators (128 columns each)
 constexpr int kEpiWarps = 16;                   // 4 per TMEM lane quarter: (channel half, tile parity)
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr int kTileBytes = kTok * kD * 2;       // 32 KB bf16 tile
@@ -40,7 +50,7 @@ struct TcSmem {
   alignas(1024) uint8_t A[kStages][kTileBytes]; // [stage][2 k-chunks][128 rows tok][128 B]
   alignas(16) uint8_t vstage[2][4][kVStage];    // per (tile parity, lane quarter): FORMAT-ordered V codes
   float2 xch[2][2][4][2][32];                   // G = 128: (buffer, parity, quarter, half, lane) min/max
-  uint64_t full[kStages], empty[kStages], tfull[2], tempty[2];
+  uint64_t full[kStages], empty[kStages], tfull[kAcc], tempty[kAcc];
   uint32_t tmem_base;
 };
 
@@ -126,9 +136,9 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
   }
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) { mbar_init(&S.full[s], 1); mbar_init(&S.empty[s], 1); }
-    for (int a = 0; a < 2; ++a) { mbar_init(&S.tfull[a], 1); mbar_init(&S.tempty[a], kEpiWarps / 2); }
+    for (int a = 0; a < kAcc; ++a) { mbar_init(&S.tfull[a], 1); mbar_init(&S.tempty[a], kEpiWarps / 2); }
   }
-  if (warp == 1) tmem_alloc(&S.tmem_base, 256);
+  if (warp == 1) tmem_alloc(&S.tmem_base, 128 * kAcc);
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // B writes -> async proxy
   fence_before();
   __syncthreads();
@@ -146,13 +156,20 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
         const int tok0 = (sub + i * p.cpp) * kTok;
         tma_load_3d(S.A[s], map, 0, h, tok0, &S.full[s]);
         tma_load_3d(S.A[s] + kTileBytes / 2, map, 64, h, tok0, &S.full[s]);
+        if (OSCAR_APPEND_L2PF > 0 && i + OSCAR_APPEND_L2PF < ntiles) {
+          // the ring holds only kStages tiles: pull the tile OSCAR_APPEND_L2PF ahead into L2 so
+          // its TMA load later sees L2 rather than DRAM latency
+          const int tokp = (sub + (i + OSCAR_APPEND_L2PF) * p.cpp) * kTok;
+          tma_prefetch_3d(map, 0, h, tokp);
+          tma_prefetch_3d(map, 64, h, tokp);
+        }
       }
     }
   } else if (warp == 1) {
     // ================= MMA issuer
     for (int i = 0; i < (MODE == 2 ? 0 : ntiles); ++i) {
-      const int s = i % kStages, a = i & 1;
-      mbar_wait(&S.tempty[a], ((i >> 1) & 1) ^ 1);
+      const int s = i % kStages, a = i % kAcc;
+      mbar_wait(&S.tempty[a], ((i / kAcc) & 1) ^ 1);
       mbar_wait(&S.full[s], (i / kStages) & 1);
       fence_after();
       if (lane == 0) {
@@ -195,14 +212,14 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
     };
     int64_t slot_next = load_slot(par);
     for (int i = par; i < ntiles; i += 2) {
-      const int a = par;
+      const int a = i % kAcc;
       const int64_t slot = slot_next;
       slot_next = load_slot(i + 2);
       uint32_t v[64];
       if constexpr (MODE == 3) {
         // z = x·U·H_128 for this row: stride-64 butterfly from both halves' TMEM columns (32 at a
         // time), then the 64-point transform of this half in registers
-        mbar_wait(&S.tfull[a], (i >> 1) & 1);
+        mbar_wait(&S.tfull[a], (i / kAcc) & 1);
         fence_after();
         const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + a * 128;
         float y[64];
@@ -242,7 +259,7 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
         continue;
       }
       if constexpr (MODE != 2) {
-        mbar_wait(&S.tfull[a], (i >> 1) & 1);
+        mbar_wait(&S.tfull[a], (i / kAcc) & 1);
         fence_after();
         const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + a * 128 + half * 64;
         OSCAR_TMEM_LD32(taddr, v);
@@ -313,6 +330,24 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
       };
 #pragma unroll
       for (int gi = 0; gi < GPH; ++gi) {
+#if OSCAR_TREE_MINMAX
+        // min / max as balanced trees (depth log2 GH instead of a GH-long dependency chain)
+        float tmn[GH / 2], tmx[GH / 2];
+#pragma unroll
+        for (int c = 0; c < GH / 2; ++c) {
+          const float x0 = __uint_as_float(v[gi * GH + 2 * c]), x1 = __uint_as_float(v[gi * GH + 2 * c + 1]);
+          tmn[c] = fminf(x0, x1);
+          tmx[c] = fmaxf(x0, x1);
+        }
+#pragma unroll
+        for (int w = GH / 4; w >= 1; w >>= 1)
+#pragma unroll
+          for (int c = 0; c < w; ++c) {
+            tmn[c] = fminf(tmn[c], tmn[c + w]);
+            tmx[c] = fmaxf(tmx[c], tmx[c + w]);
+          }
+        float mn = tmn[0], mx = tmx[0];
+#else
         float mn = __uint_as_float(v[gi * GH]), mx = mn;
 #pragma unroll
         for (int c = 1; c < GH; ++c) {
@@ -320,6 +355,7 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
           mn = fminf(mn, x);
           mx = fmaxf(mx, x);
         }
+#endif
         if (G == 128) {
           // the group spans both channel halves: swap min/max with the partner warp (same rows)
           S.xch[xbuf][par][quarter][half][lane] = make_float2(mn, mx);
@@ -423,7 +459,7 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
   __syncthreads();
   if (warp == 1) {
     fence_after();
-    tmem_dealloc(tmem, 256);
+    tmem_dealloc(tmem, 128 * kAcc);
   }
 }
 

@@ -185,7 +185,6 @@ attend_partial_mma(AttnParams p, int S) {
   // G = 32, g = 4 (PVG too): M-tile pair p takes V words 2p (rows gid: group 2p) / 2p + 1 (rows
   // gid + 8: group 2p + 1); its 8 columns are the 4 heads of group 2p, then of group 2p + 1
   constexpr bool PVG = TQ && ((GQ == 8 && NG == 2) || (GQ == 4 && NG == 4));
-  static_assert(!(PVG && BITS == 3), "3-bit token-row layout: combo-tile PV only");
   // 3-bit codes (reading Z36): a 2-bit low plane in the 2-bit places plus a 1-bit high plane;
   // LB = bits of the low plane every in-place operand below is built from
   constexpr int LB = BITS == 3 ? 2 : BITS;
@@ -581,6 +580,7 @@ attend_partial_mma(AttnParams p, int S) {
           // one ldmatrix.x4: matrices (rows 0-7 | 8-15) x (bytes 0-15 | 16-31) of the K tile, so
           // lane (gid, t) receives words t and 4 + t of rows gid and gid + 8
           uint32_t wa[NG == 4 ? 8 : 2], wb[NG == 4 ? 8 : 2];
+          uint32_t ha4[NG == 4 && BITS == 3 ? 4 : 1], hb4[NG == 4 && BITS == 3 ? 4 : 1];
           if constexpr (NG == 4) {
             // G = 32: lane t takes 2-bit field t of every word of rows gid / gid + 8 (k-step g =
             // words 2g, 2g + 1 = group g)
@@ -591,6 +591,11 @@ attend_partial_mma(AttnParams p, int S) {
             wa[4] = a1.x; wa[5] = a1.y; wa[6] = a1.z; wa[7] = a1.w;
             wb[0] = b0.x; wb[1] = b0.y; wb[2] = b0.z; wb[3] = b0.w;
             wb[4] = b1.x; wb[5] = b1.y; wb[6] = b1.z; wb[7] = b1.w;
+            if constexpr (BITS == 3) {           // the 4 high-plane words of both rows
+              const uint4 a2 = ra[2], b2 = rb[2];
+              ha4[0] = a2.x; ha4[1] = a2.y; ha4[2] = a2.z; ha4[3] = a2.w;
+              hb4[0] = b2.x; hb4[1] = b2.y; hb4[2] = b2.z; hb4[3] = b2.w;
+            }
           } else {
             const int mi = lane >> 3;
             const uint32_t addr = smem_u32(pg + (size_t)(16 * st + 8 * (mi >> 1) + (lane & 7)) * RB + 16 * (mi & 1));
@@ -601,7 +606,7 @@ attend_partial_mma(AttnParams p, int S) {
           // 3-bit: the high-plane words of low words t and 4 + t (high word j / 2, nibble j % 2
           // = t % 2) of rows gid / gid + 8, normalized so the lane's nibble sits in bits 4-7
           uint32_t ha[2], hb[2];
-          if constexpr (BITS == 3) {
+          if constexpr (BITS == 3 && NG != 4) {
             const uint32_t* ra = reinterpret_cast<const uint32_t*>(pg + (size_t)(16 * st + gid) * RB + 32);
             const uint32_t* rb = reinterpret_cast<const uint32_t*>(pg + (size_t)(16 * st + 8 + gid) * RB + 32);
             const int sh = (t & 1) ? 0 : 4;
@@ -618,7 +623,14 @@ attend_partial_mma(AttnParams p, int S) {
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
             uint32_t a[4];
-            if constexpr (NG == 4) {
+            if constexpr (NG == 4 && BITS == 3) {
+              // 3-bit, G = 32: field t to bits 5-6 (lo·32)
+              auto lo5 = [&](uint32_t w) { return (t < 3 ? (w << (5 - 2 * t)) : (w >> 1)) & 0x60606060u; };
+              a[0] = lo5(wa[2 * kk]);
+              a[1] = lo5(wb[2 * kk]);
+              a[2] = lo5(wa[2 * kk + 1]);
+              a[3] = lo5(wb[2 * kk + 1]);
+            } else if constexpr (NG == 4) {
               // k-step kk = group kk: field t of words 2kk (a0, a1) and 2kk + 1 (a2, a3)
               const uint32_t mul = 1u << (6 - 2 * t);
               a[0] = (wa[2 * kk] * mul) & 0xC0C0C0C0u;
@@ -653,12 +665,20 @@ attend_partial_mma(AttnParams p, int S) {
             for (int jt = 0; jt < NTQ; ++jt) imma16832_us(cq[jt][g], a, bq[jt][kk][0], bq[jt][kk][1]);
             if constexpr (BITS == 3) {
               // the high bit to bit 7 (hi·128): code·32 = lo·32 + hi·128 into the same C
-              const int wi = kk >> 1, f0 = 2 * (kk & 1);
               uint32_t ah[4];
-              ah[0] = (ha[wi] << (3 - f0)) & 0x80808080u;
-              ah[1] = (hb[wi] << (3 - f0)) & 0x80808080u;
-              ah[2] = (ha[wi] << (2 - f0)) & 0x80808080u;
-              ah[3] = (hb[wi] << (2 - f0)) & 0x80808080u;
+              if constexpr (NG == 4) {
+                // low words 2kk (even: high bit t) and 2kk + 1 (odd: 4 + t) -> high word kk
+                ah[0] = (ha4[kk] << (7 - t)) & 0x80808080u;
+                ah[1] = (hb4[kk] << (7 - t)) & 0x80808080u;
+                ah[2] = (ha4[kk] << (3 - t)) & 0x80808080u;
+                ah[3] = (hb4[kk] << (3 - t)) & 0x80808080u;
+              } else {
+                const int wi = kk >> 1, f0 = 2 * (kk & 1);
+                ah[0] = (ha[wi] << (3 - f0)) & 0x80808080u;
+                ah[1] = (hb[wi] << (3 - f0)) & 0x80808080u;
+                ah[2] = (ha[wi] << (2 - f0)) & 0x80808080u;
+                ah[3] = (hb[wi] << (2 - f0)) & 0x80808080u;
+              }
 #pragma unroll
               for (int jt = 0; jt < NTQ; ++jt) imma16832_us(cq[jt][g], ah, bq[jt][kk][0], bq[jt][kk][1]);
             }
@@ -799,6 +819,15 @@ attend_partial_mma(AttnParams p, int S) {
               a[2] = vs[pg2] & msk;
               a[3] = vs[pg2 + 1] & msk;
               hmma16816(acc[i][0], a, bpv[i / CPB][0], bpv[i / CPB][1]);
+              if constexpr (BITS == 3) {
+                const uint32_t mh = 0x00040004u << (2 * q);
+                uint32_t ah[4];
+                ah[0] = (vh[pg2] << (q + 2)) & mh;
+                ah[1] = (vh[pg2 + 1] << (q + 2)) & mh;
+                ah[2] = (vh[pg2] >> (6 - q)) & mh;
+                ah[3] = (vh[pg2 + 1] >> (6 - q)) & mh;
+                hmma16816(acc[i][0], ah, bpv[i / CPB][0], bpv[i / CPB][1]);
+              }
             } else {
               a[0] = vw[i / CPB] & msk;
               a[1] = vw[VW / 2 + i / CPB] & msk;
@@ -950,11 +979,12 @@ KernelFn pick_tq(int g, int ng) {
   return nullptr;
 }
 
-// 3-bit (reading Z36 planes) on the token-row layout: the combo-tile PV shapes
+// 3-bit (reading Z36 planes) on the token-row layout: the same shapes as 2-bit
 KernelFn pick_tq3(int g, int ng) {
 #define OSCAR_CASE(GQ_, NG_) \
   if (g == GQ_ && ng == NG_) return attend_partial_mma<3, GQ_, NG_, true>;
-  OSCAR_CASE(2, 1) OSCAR_CASE(2, 2) OSCAR_CASE(4, 1) OSCAR_CASE(4, 2) OSCAR_CASE(8, 1)
+  OSCAR_CASE(2, 1) OSCAR_CASE(2, 2) OSCAR_CASE(4, 1) OSCAR_CASE(4, 2) OSCAR_CASE(4, 4) OSCAR_CASE(8, 1)
+  OSCAR_CASE(8, 2)
 #undef OSCAR_CASE
   return nullptr;
 }

@@ -293,6 +293,8 @@ def _z31_lse_bound(q, pt, L, pool, RK, fmt, Hkv):
     dict(name="b3G32", Hq=8, Hkv=2, bits=3, G=32, B=2, L=[290, 17]),
     dict(name="b3G128", Hq=16, Hkv=2, bits=3, G=128, B=2, L=[300, 64]),
     dict(name="b4g8", Hq=16, Hkv=2, bits=4, G=64, B=2, L=[250, 1]),
+    dict(name="b3g8G64", Hq=16, Hkv=2, bits=3, G=64, B=2, L=[400, 70]),    # 3-bit, group-pure PV tiles
+    dict(name="b3C2", Hq=32, Hkv=8, bits=3, G=64, B=3, L=[1000, 77, 0]),   # 3-bit token-row layout
 ])
 @pytest.mark.parametrize("variant", [0, 1])
 @pytest.mark.parametrize("pps", [0, 1, 3])

@@ -138,6 +138,25 @@ def cpu_threads():
     return 1
 
 
+# The JSON line goes to the process's original stdout; everything else written to fd 1 (library
+# banners such as NCCL's version line) is sent to stderr, so stdout carries exactly one line.
+_JSON_OUT = None
+
+
+def claim_stdout():
+    global _JSON_OUT
+    if _JSON_OUT is None:
+        sys.stdout.flush()
+        _JSON_OUT = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)
+
+
+def emit(obj):
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    out.write(json.dumps(obj) + "\n")
+    out.flush()
+
+
 # ------------------------------------------------------------------ reference (CPU oracle) arm
 def run_reference(args, rank):
     if rank != 0:
@@ -174,7 +193,7 @@ def run_reference(args, rank):
                                    "of the C2 decode workload (1/128 of one layer-step)"},
         "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def workload_config(args):
@@ -409,6 +428,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the oracle (cpu_baseline) legs")
     ap.add_argument("--no-graph", action="store_true", help="time the step as plain stream launches only")
     args = ap.parse_args()
+    claim_stdout()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -443,7 +463,7 @@ def main():
     hbm_peak, _, peak_kind = measured_peaks()
     if args.c5_only:
         if rank == 0:
-            print(json.dumps(c5_leg(args, dev, hbm_peak)), flush=True)
+            emit(c5_leg(args, dev, hbm_peak))
         return
     if args.c4_only:
         gen = torch.Generator(device=dev).manual_seed(1234 + rank)
@@ -451,7 +471,7 @@ def main():
         RV = torch.stack([synth.torch_rotation(gen, HKV, D, dev) for _ in range(C4_LAYERS)])
         r = c4_leg(args, world, rank, dev, gen, RK, RV, hbm_peak, peak_kind)
         if rank == 0:
-            print(json.dumps(r), flush=True)
+            emit(r)
         return
     o = Bnd.Oscar(Bnd.Config(num_q_heads=HQ, num_kv_heads=HKV, bits=BITS, group_size=G, page_size=P))
     o.set_variant(args.variant)
@@ -805,7 +825,7 @@ def main():
         line["cpu_baseline"] = cpu
     line.update(extras)
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
     if dist.is_initialized():
         dist.destroy_process_group()
 

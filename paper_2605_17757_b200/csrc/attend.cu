@@ -6,10 +6,12 @@
 //                          (split, kv head, sequence)); the tensor-core kernel is in
 //                          attend_mma.cu (variant 0)
 //   attend_merge_kernel    LSE merge over splits, o = õ · R_Vᵀ, bf16/fp32 store, lse
+#include <algorithm>
 #include <type_traits>
 #include "common.cuh"
 #include "attend_common.cuh"
 #include "append_epilogue.cuh"
+#include "ptx.cuh"
 
 #ifndef OSCAR_PDL_MERGE
 #define OSCAR_PDL_MERGE 1
@@ -28,11 +30,21 @@ namespace oscar {
 //     32639, qint = rint(q̃/qscale) (|qint| <= 32639 = 127·256 + 127, so the hi/lo int8 split
 //     never overflows), qsum[grp] = Σ_{c in grp} qint; then all threads write the per-lane IMMA
 //     operand fragments of the group.
-// (The decode step's QuantizeAndWrite of the new K/V row runs in the merge kernel, off the
-// partial kernel's critical path — see attend_merge_kernel.)
-// PDL: launched as an ordinary kernel (every earlier kernel of the stream is complete when it
-// starts) and lets the partial kernel launch at once; the partial kernel's early page prefetch
-// only reads pool pages, which nothing in this call writes before the merge kernel.
+// Decode step (oscar_decode_step; Alg. 1 DecodeStep P:L1627-1635, reading Z35): the step's new
+// K / V rows ride along as two more rows of the same contraction (x̃_K = k·R_K, x̃_V = v·R_V), then
+// warps GQ / GQ + 1 run QuantizeAndWrite of the K / V row (shared clip/min-max/pack
+// epilogue, store at slot page_table[b][(L-1)/P]·P + (L-1)%P) and leave the DEQUANTIZED rows
+// k̂, v̂ (exactly what the pool now holds) in the workspace (newtok); the merge kernel folds the
+// new token in as one more partial (logit q̃·k̂, weight 1, value v̂).  Same result as appending
+// first and attending over seq_len tokens.  The partial kernels attend over the first
+// seq_len - 1 tokens only: the slot written here lies past every token they use (masked), so
+// their early page prefetch may overlap this store.
+// PDL: launched behind whatever precedes it on the stream; R_K[h] / R_V[h] are bulk-copied to smem
+// before griddepcontrol.wait (rotations are never produced by a kernel that triggers its dependents
+// early — none of this library's kernels that do write them, and a kernel without the trigger
+// completes before this one launches), q, the new rows and the page table after it.  It then
+// lets the partial kernel launch at once; the partial kernel's early page prefetch only reads
+// pool pages.
 struct PrologueParams {
   const uint16_t* q;            // [B][H_q][128] bf16
   const float* RK;              // [H_kv][128][128]
@@ -45,66 +57,135 @@ struct PrologueParams {
   uint32_t* qfrag;              // null: simple kernel path
   int tq;                       // 1: fragments for the token-row QK layout of attend_partial_mma
   int32_t* work;                // null: simple kernel path
+  const uint16_t* knew;         // decode step: [B][H_kv][128] bf16 new K / V rows (null: attend)
+  const uint16_t* vnew;
+  const float* RV;              // [H_kv][128][128]; null: pre-rotated V (identity)
+  float* newtok;                // decode step: [B][H_kv][2][128] fp32 k̂, v̂
+  const int32_t* page_table;    // decode step: slot of the new row
+  const int32_t* seq_lens;
+  int max_pages;
+  uint8_t* pool;
+  EpiParams ep;
   unsigned long long* tl;       // timing probe (OSCAR_PROBE_TL)
 };
 
 template <int GQ>
 __global__ void __launch_bounds__(512) attend_prologue_kernel(PrologueParams pp) {
-  constexpr int NR = GQ;                             // q heads
-  extern __shared__ __align__(16) float psm[];
-  float* ps = psm;                                   // [16][NR][128] partial dots
+  constexpr int NR = GQ + 2;                         // q heads, then the decode step's K and V rows
+  // dynamic smem: R_K[h] (64 KB) then R_V[h] (64 KB, decode step), bulk-copied before the wait;
+  // the [16][NR][128] partial dots reuse it once every warp has finished its dots
+  extern __shared__ __align__(128) float psm[];
+  float* Rks = psm;
+  float* Rvs = psm + kD * kD;
+  float* ps = psm;
   __shared__ __align__(16) float xs[NR][kD];         // input rows (fp32)
   __shared__ __align__(16) float ys[NR][kD];         // rotated rows
   __shared__ int16_t qis[GQ][kD];
-  // launched with PDL behind whatever precedes it on the stream: wait for it first (q, R_K and
-  // the pool may be its outputs), then let the partial kernel launch
+  __shared__ __align__(8) uint64_t rbar;
+  const int b = blockIdx.x, h = blockIdx.y, tid = threadIdx.x;
+  const int w = tid >> 5, lane = tid & 31;
+  const bool step = pp.knew != nullptr;
+  const bool rotv = step && pp.RV != nullptr;
   if (threadIdx.x == 0) tl_mark(pp.tl, 0, blockIdx.y * gridDim.x + blockIdx.x, 0);
+  // R_K[h] (and R_V[h] for the decode step's V row) into smem: issued before the wait
+  if (tid == 0) {
+    constexpr uint32_t bytes = kD * kD * 4;
+    ptx::mbar_init(&rbar, 1);
+    ptx::mbar_init_fence();
+    ptx::mbar_expect_tx(&rbar, rotv ? 2 * bytes : bytes);
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                 ::"r"(ptx::su32(Rks)), "l"(pp.RK + (size_t)h * kD * kD), "r"(bytes), "r"(ptx::su32(&rbar)) : "memory");
+    if (rotv)
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                   ::"r"(ptx::su32(Rvs)), "l"(pp.RV + (size_t)h * kD * kD), "r"(bytes), "r"(ptx::su32(&rbar)) : "memory");
+  }
+  // launched with PDL behind whatever precedes it on the stream: wait for it before reading q and
+  // the new rows (they may be its outputs), then let the partial kernel launch
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   if (threadIdx.x == 0) tl_mark(pp.tl, 0, blockIdx.y * gridDim.x + blockIdx.x, 1);
-  const int b = blockIdx.x, h = blockIdx.y, tid = threadIdx.x;
-  const int w = tid >> 5, lane = tid & 31;
   const int G = 1 << pp.lgG;
   if (pp.work && b == 0 && h == 0 && tid == 0) *pp.work = 0;   // reset the work-item counter
+  // decode step: the new row's slot (warps GQ, GQ + 1), its loads overlapping the rotation
+  int Lstep = 0;
+  int64_t slot = 0;
+  if (step && (w == GQ || w == GQ + 1)) {
+    Lstep = pp.seq_lens[b];
+    if (Lstep > 0) {
+      const int pos = Lstep - 1;
+      slot = (int64_t)pp.page_table[(size_t)b * pp.max_pages + pos / pp.ep.P] * pp.ep.P + pos % pp.ep.P;
+    }
+  }
 #ifdef OSCAR_PROBE_NOPRO
   return;                                            // timing probe only (results invalid)
 #endif
-  // this warp's 8 rows of R_K are loaded first: their latency overlaps the row loads
-  float4 rk[8];
-  {
-    const float4* RK4 = reinterpret_cast<const float4*>(pp.RK + (size_t)h * kD * kD) + (size_t)8 * w * 32 + lane;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) rk[i] = __ldg(RK4 + i * 32);
-  }
-  for (int e = tid; e < NR * (kD / 4); e += 512) {
+  const int nrow = step ? NR : GQ;
+  for (int e = tid; e < nrow * (kD / 4); e += 512) {
     const int r = e >> 5, l4 = e & 31;
-    const uint16_t* src = pp.q + ((size_t)b * pp.Hq + (size_t)h * GQ + r) * kD;
+    const uint16_t* src = r < GQ ? pp.q + ((size_t)b * pp.Hq + (size_t)h * GQ + r) * kD
+                                 : (r == GQ ? pp.knew : pp.vnew) + ((size_t)b * gridDim.y + h) * kD;
     const uint2 u = reinterpret_cast<const uint2*>(src)[l4];
     reinterpret_cast<float4*>(xs[r])[l4] =
         make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xffff0000u),
                     __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xffff0000u));
   }
   __syncthreads();
+  ptx::mbar_wait(&rbar, 0);                          // R_K (R_V) resident
+  // warp w contracts rows 8w..8w+7 of R (lane: columns 4l..4l+3)
+  float4 acc[NR];
+#pragma unroll
+  for (int r = 0; r < NR; ++r) acc[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float4 mk = reinterpret_cast<const float4*>(Rks + (size_t)(8 * w + i) * kD)[lane];
+#pragma unroll
+    for (int r = 0; r < GQ + 1; ++r) {
+      if (r == GQ && !step) break;
+      const float x = xs[r][8 * w + i];
+      acc[r].x = fmaf(x, mk.x, acc[r].x); acc[r].y = fmaf(x, mk.y, acc[r].y);
+      acc[r].z = fmaf(x, mk.z, acc[r].z); acc[r].w = fmaf(x, mk.w, acc[r].w);
+    }
+    if (rotv) {
+      const float4 mv = reinterpret_cast<const float4*>(Rvs + (size_t)(8 * w + i) * kD)[lane];
+      const float x = xs[GQ + 1][8 * w + i];
+      acc[GQ + 1].x = fmaf(x, mv.x, acc[GQ + 1].x); acc[GQ + 1].y = fmaf(x, mv.y, acc[GQ + 1].y);
+      acc[GQ + 1].z = fmaf(x, mv.z, acc[GQ + 1].z); acc[GQ + 1].w = fmaf(x, mv.w, acc[GQ + 1].w);
+    }
+  }
+  __syncthreads();                                   // every warp is done with R: ps reuses it
 #pragma unroll
   for (int r = 0; r < NR; ++r) {
-    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const float x = xs[r][8 * w + i];
-      const float4 m = rk[i];
-      a.x = fmaf(x, m.x, a.x); a.y = fmaf(x, m.y, a.y); a.z = fmaf(x, m.z, a.z); a.w = fmaf(x, m.w, a.w);
-    }
-    reinterpret_cast<float4*>(ps + ((size_t)w * NR + r) * kD)[lane] = a;
+    if (r >= GQ && !step) break;
+    if (r == GQ + 1 && !rotv) break;
+    reinterpret_cast<float4*>(ps + ((size_t)w * NR + r) * kD)[lane] = acc[r];
   }
   __syncthreads();
-  for (int e = tid; e < NR * kD; e += 512) {
+  for (int e = tid; e < nrow * kD; e += 512) {
     const int r = e >> 7, c = e & (kD - 1);
     float y = 0.f;
+    if (r == GQ + 1 && !rotv) {
+      y = xs[r][c];                                  // pre-rotated V (NEXT-2): identity
+    } else {
 #pragma unroll
-    for (int ww = 0; ww < 16; ++ww) y += ps[((size_t)ww * NR + r) * kD + c];
+      for (int ww = 0; ww < 16; ++ww) y += ps[((size_t)ww * NR + r) * kD + c];
+    }
     ys[r][c] = y;
   }
   __syncthreads();
+  if (step && (w == GQ || w == GQ + 1)) {
+    // QuantizeAndWrite of the new K (warp GQ) / V (warp GQ + 1) row; its dequantized row k̂ / v̂
+    // goes to newtok for the merge kernel.  These two warps are done after this: the rest of
+    // the CTA synchronises without them (named barrier 1), so this chain overlaps the q path.
+    const int isV = w - GQ;
+    if (Lstep > 0) {
+      const float4 y4 = reinterpret_cast<const float4*>(ys[GQ + isV])[lane];
+      float yy[4] = {y4.x, y4.y, y4.z, y4.w}, dq[4];
+      quantize_store_row_warp(pp.ep, yy, lane, slot, h, isV, pp.pool, dq);
+      reinterpret_cast<float4*>(pp.newtok + (((size_t)b * gridDim.y + h) * 2 + isV) * kD)[lane] =
+          make_float4(dq[0], dq[1], dq[2], dq[3]);
+    }
+    return;
+  }
   if (w < GQ) {
     const size_t row = (size_t)b * pp.Hq + (size_t)h * GQ + w;
     float4 a = reinterpret_cast<const float4*>(ys[w])[lane];
@@ -127,7 +208,10 @@ __global__ void __launch_bounds__(512) attend_prologue_kernel(PrologueParams pp)
     for (int o = 1; o < (G >> 2); o <<= 1) gs += __shfl_xor_sync(0xffffffffu, gs, o);
     if ((lane & ((G >> 2) - 1)) == 0) pp.qsum[row * 8 + (lane * 4 >> pp.lgG)] = gs;
   }
-  __syncthreads();
+  if (step) asm volatile("bar.sync 1, %0;\n" ::"r"(512 - 64) : "memory");   // all but warps GQ, GQ + 1
+  else __syncthreads();
+  // the fragment writers: every thread still running, renumbered 0 .. nft - 1
+  const int ft = step && w > GQ + 1 ? tid - 64 : tid, nft = step ? 512 - 64 : 512;
   // IMMA A fragments for attend_partial_mma: word (j, kk, r) of lane (gid, t) holds the
   // hi (r even) / lo (r odd) int8 of qint[head][channel] for combo 8j + gid = grp·g + head,
   // zero outside the combo's group (see attend_mma.cu)
@@ -138,7 +222,7 @@ __global__ void __launch_bounds__(512) attend_prologue_kernel(PrologueParams pp)
     // for kk < 2 or >= 2
     constexpr int NTQ = (GQ + 3) / 4;
     uint32_t* dst = pp.qfrag + ((size_t)b * gridDim.y + h) * NTQ * 8 * 32;
-    for (int wd = tid; wd < NTQ * 8 * 32; wd += 512) {
+    for (int wd = ft; wd < NTQ * 8 * 32; wd += nft) {
       const int ln = wd & 31, rest = wd >> 5;
       const int r = rest & 1, kk = (rest >> 1) & 3, jt = rest >> 3;
       const int gid = ln >> 2, t = ln & 3;
@@ -162,7 +246,7 @@ __global__ void __launch_bounds__(512) attend_prologue_kernel(PrologueParams pp)
   } else if (pp.qfrag) {
     const int nc = GQ << (7 - pp.lgG);
     uint32_t* dst = pp.qfrag + ((size_t)b * gridDim.y + h) * pp.nt * 16 * 32;
-    for (int wd = tid; wd < pp.nt * 16 * 32; wd += 512) {
+    for (int wd = ft; wd < pp.nt * 16 * 32; wd += nft) {
       const int ln = wd & 31, rest = wd >> 5;
       const int r = rest & 3, kk = (rest >> 2) & 3, j = rest >> 4;
       const int gid = ln >> 2, t = ln & 3, cb = 8 * j + gid;
@@ -182,7 +266,7 @@ __global__ void __launch_bounds__(512) attend_prologue_kernel(PrologueParams pp)
       dst[wd] = v;
     }
   }
-  if (threadIdx.x == 0) tl_mark(pp.tl, 0, blockIdx.y * gridDim.x + blockIdx.x, 2);
+  if (ft == 0) tl_mark(pp.tl, 0, blockIdx.y * gridDim.x + blockIdx.x, 2);
 }
 
 // ------------------------------------------------------------------ simple partial kernel
@@ -398,14 +482,9 @@ __global__ void __launch_bounds__(128) attend_partial_simple(AttnParams p) {
 // thread (c', half) forms output channel c' of every other head from smem, the contraction index
 // rotated by lane (c = 4·((k + lane) mod 32)) so the 32 rows of a warp hit distinct banks.
 //
-// Decode step (Alg. 1 DecodeStep; reading Z35): the partial kernel attends over the
-// first seq_len - 1 tokens of the pool; this kernel, BEFORE griddepcontrol.wait (so the work
-// overlaps the partial kernel's tail), runs QuantizeAndWrite of the step's new K/V
-// row — x̃ = x·R (warp w contracts rows 16w..16w+15 of R_K from L2 / R_V from smem), the shared
-// clip/min-max/pack epilogue, store at slot page_table[b][(L-1)/P]·P + (L-1)%P (one CTA per
-// (b, h) stores) — and folds the new token as one more partial: logit q̃·k̂ of its DEQUANTIZED
-// key (k̂ = s16·c + m16, exactly what the pool now holds), weight 1, value v̂.  Same result as
-// appending first and attending over seq_len tokens.
+// Decode step (Alg. 1 DecodeStep; reading Z35): the prologue has stored the step's
+// new K/V row (QuantizeAndWrite) and left its dequantized rows k̂, v̂ in the workspace (newtok);
+// this kernel folds the new token in as one more partial: logit q̃·k̂, weight 1, value v̂.
 namespace {
 __device__ __forceinline__ uint32_t msmem_u32(const void* ptr) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(ptr));
@@ -413,14 +492,8 @@ __device__ __forceinline__ uint32_t msmem_u32(const void* ptr) {
 }  // namespace
 
 struct StepParams {
-  const uint16_t* knew;         // [B][H_kv][128] bf16; null: plain attend
-  const uint16_t* vnew;
-  const float* RK;              // [H_kv][128][128]
-  const int32_t* page_table;
+  int step;                     // 1: decode step (the prologue appended the new row)
   const int32_t* seq_lens;
-  int max_pages;
-  uint8_t* pool;
-  EpiParams ep;
 };
 
 template <int HC>
@@ -436,7 +509,7 @@ __global__ void __launch_bounds__(256) attend_merge_kernel(AttnParams p, const f
   extern __shared__ __align__(128) float Rs[];       // [128][128] R_V[h]
   __shared__ __align__(16) float po[8][kD];
   __shared__ __align__(16) float ot[HC][kD];
-  __shared__ __align__(16) float nrow[2][kD];        // decode step: new K / V row, then k̂ / v̂
+  __shared__ __align__(16) float vhat[kD];           // decode step: v̂ of the new token
   __shared__ float pm[8], pl[8], sws[HC], nlog[HC];
   __shared__ __align__(8) uint64_t bar;
   const int b = blockIdx.x, h = blockIdx.y, tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
@@ -463,81 +536,16 @@ __global__ void __launch_bounds__(256) attend_merge_kernel(AttnParams p, const f
         "@!P1 bra WAIT_R%=;\n}\n" ::"r"(msmem_u32(&bar))
         : "memory");
   };
-  // ---- decode step: QuantizeAndWrite of the new row + its attention partial (pre-wait)
-  const int Lnew = sp.knew ? sp.seq_lens[b] : 0;
+  // ---- decode step: the new token's partial — logit q̃·k̂ (log2 units) per head, value v̂; k̂, v̂
+  // from the prologue (newtok)
+  const int Lnew = sp.step ? sp.seq_lens[b] : 0;
   if (Lnew > 0) {
-    __syncthreads();                                 // bar initialised before anyone waits on it
-    if (w < 2) {
-      const uint16_t* src = (w ? sp.vnew : sp.knew) + ((size_t)b * p.hkv + h) * kD;
-      const uint2 u = reinterpret_cast<const uint2*>(src)[lane];
-      reinterpret_cast<float4*>(nrow[w])[lane] =
-          make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xffff0000u),
-                      __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xffff0000u));
-    }
-    __syncthreads();
-    // x̃ partial dots: warp w contracts rows 16w..16w+15 (lane: columns 4l..4l+3); K with R_K
-    // from L2 (16 float4 in flight), V with R_V from smem (identity when R_V = NULL)
-    {
-      const float4* RK4 = reinterpret_cast<const float4*>(sp.RK + (size_t)h * kD * kD) + (size_t)16 * w * 32 + lane;
-      float4 rk[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) rk[i] = __ldg(RK4 + i * 32);
-      float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const float x = nrow[0][16 * w + i];
-        a.x = fmaf(x, rk[i].x, a.x); a.y = fmaf(x, rk[i].y, a.y); a.z = fmaf(x, rk[i].z, a.z); a.w = fmaf(x, rk[i].w, a.w);
-      }
-      reinterpret_cast<float4*>(po[w])[lane] = a;
-    }
-    float4 av = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (RV) {
-      wait_rv();
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const float x = nrow[1][16 * w + i];
-        const float4 r = reinterpret_cast<const float4*>(Rs + (size_t)(16 * w + i) * kD)[lane];
-        av.x = fmaf(x, r.x, av.x); av.y = fmaf(x, r.y, av.y); av.z = fmaf(x, r.z, av.z); av.w = fmaf(x, r.w, av.w);
-      }
-    }
-    __syncthreads();
-    float y = 0.f;                                   // thread c (< 128): x̃_K[c]; 128 + c: x̃_V[c]
-    {
-      const int c = tid & (kD - 1);
-      if (tid < kD) {
-#pragma unroll
-        for (int ww = 0; ww < 8; ++ww) y += po[ww][c];
-      }
-    }
-    __syncthreads();
-    reinterpret_cast<float4*>(po[w])[lane] = av;     // V partials reuse po
-    __syncthreads();
-    if (tid >= kD) {
-      const int c = tid - kD;
-      if (RV) {
-#pragma unroll
-        for (int ww = 0; ww < 8; ++ww) y += po[ww][c];
-      } else {
-        y = nrow[1][c];                              // pre-rotated V (NEXT-2): identity
-      }
-    }
-    __syncthreads();
-    nrow[tid >> 7][tid & (kD - 1)] = y;
-    __syncthreads();
-    if (w < 2) {                                     // warp 0: K row, warp 1: V row
-      const int pos = Lnew - 1;
-      const int64_t slot = (int64_t)sp.page_table[(size_t)b * sp.max_pages + pos / sp.ep.P] * sp.ep.P + pos % sp.ep.P;
-      const float4 y4 = reinterpret_cast<const float4*>(nrow[w])[lane];
-      float yy[4] = {y4.x, y4.y, y4.z, y4.w}, dq[4];
-      quantize_store_row_warp(sp.ep, yy, lane, slot, h, w, blockIdx.z == 0 ? sp.pool : nullptr, dq);
-      __syncwarp();
-      reinterpret_cast<float4*>(nrow[w])[lane] = make_float4(dq[0], dq[1], dq[2], dq[3]);
-    }
-    __syncthreads();
-    if (w < HC) {                                    // new-token logit (log2 units): q̃·k̂
+    const float* nt = p.newtok + ((size_t)b * p.hkv + h) * 2 * kD;
+    if (tid < kD / 4) reinterpret_cast<float4*>(vhat)[tid] = __ldcg(reinterpret_cast<const float4*>(nt + kD) + tid);
+    if (w < HC) {
       const size_t row = (size_t)b * p.hq + (size_t)h * p.g + hz + w;
       const float4 qv = __ldcg(reinterpret_cast<const float4*>(p.qt + row * kD) + lane);
-      const float4 kv = reinterpret_cast<const float4*>(nrow[0])[lane];
+      const float4 kv = __ldcg(reinterpret_cast<const float4*>(nt) + lane);
       float d = qv.x * kv.x + qv.y * kv.y + qv.z * kv.z + qv.w * kv.w;
       for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
       if (lane == 0) nlog[w] = d;
@@ -643,7 +651,7 @@ __global__ void __launch_bounds__(256) attend_merge_kernel(AttnParams p, const f
       if (Lnew > 0) {                                // the step's new token: weight 1, value v̂
         const float wn = exp2f(mnew - M);
         L += wn;
-        o = fmaf(nrow[1][c], wn, o);
+        o = fmaf(vhat[c], wn, o);
       }
     }
     const float wseg = (seg && M != -INFINITY) ? exp2f(p.seg_m[row] - M) : 0.f;
@@ -798,7 +806,7 @@ static int n_split_slots(const oscar_ctx& c, int B, int max_pages) {
 // Workspace carve-up: every sub-buffer starts on a 256-B boundary (the kernels use 8- and 16-B
 // vector accesses on them, and B·H_q may be odd).
 struct WsLayout {
-  size_t qt, ws_o, ws_m, ws_l, qsum, qscale, qint, qfrag, work, seg_o, seg_m, seg_l, total;
+  size_t qt, ws_o, ws_m, ws_l, qsum, qscale, qint, qfrag, work, seg_o, seg_m, seg_l, newtok, total;
 };
 static WsLayout ws_layout(const oscar_ctx& c, int B, int max_pages) {
   const size_t ns = (size_t)n_split_slots(c, B, max_pages);
@@ -823,6 +831,7 @@ static WsLayout ws_layout(const oscar_ctx& c, int B, int max_pages) {
   w.seg_o = take(rows * kD * 4);
   w.seg_m = take(rows * 4);
   w.seg_l = take(rows * 4);
+  w.newtok = take((size_t)B * c.hkv * 2 * kD * 4);
   w.total = off;
   return w;
 }
@@ -875,6 +884,7 @@ cudaError_t launch_attend(const oscar_ctx& c, const void* q, const int32_t* page
     p.qint = reinterpret_cast<int16_t*>(base + w.qint);
     p.qfrag = reinterpret_cast<uint32_t*>(base + w.qfrag);
     p.work = reinterpret_cast<int32_t*>(base + w.work);
+    p.newtok = reinterpret_cast<float*>(base + w.newtok);
     if (seg_k) {
       p.seg_o = reinterpret_cast<float*>(base + w.seg_o);
       p.seg_m = reinterpret_cast<float*>(base + w.seg_m);
@@ -895,10 +905,15 @@ cudaError_t launch_attend(const oscar_ctx& c, const void* q, const int32_t* page
     pp.qt = p.qt; pp.qint = p.qint; pp.qsc = p.qscale; pp.qsum = p.qsum;
     pp.qfrag = mma ? p.qfrag : nullptr;
     pp.tq = mma && attend_mma_tq(c) ? 1 : 0; pp.work = mma ? p.work : nullptr;
+    pp.knew = static_cast<const uint16_t*>(k_new); pp.vnew = static_cast<const uint16_t*>(v_new);
+    pp.RV = RV; pp.newtok = p.newtok;
+    pp.page_table = page_table; pp.seq_lens = seq_lens; pp.max_pages = max_pages;
+    pp.pool = static_cast<uint8_t*>(const_cast<void*>(pool));
+    pp.ep = make_epi_params(c);
     pp.tl = g_tl;
     void (*fn)(PrologueParams) = c.g == 1 ? attend_prologue_kernel<1> : c.g == 2 ? attend_prologue_kernel<2>
                                : c.g == 4 ? attend_prologue_kernel<4> : attend_prologue_kernel<8>;
-    const int psmem = 16 * c.g * kD * (int)sizeof(float);
+    const int psmem = std::max(16 * (c.g + 2) * kD, (k_new && RV ? 2 : 1) * kD * kD) * (int)sizeof(float);
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, psmem);
     if (e != cudaSuccess) return e;
     // PDL launch: its CTAs may become resident while the previous kernel of the stream drains;
@@ -952,10 +967,8 @@ cudaError_t launch_attend(const oscar_ctx& c, const void* q, const int32_t* page
     const int hc = per_head ? 1 : c.g;
     const int msmem = RV ? kD * kD * 4 : 0;
     StepParams sp{};
-    sp.knew = static_cast<const uint16_t*>(k_new); sp.vnew = static_cast<const uint16_t*>(v_new);
-    sp.RK = RK; sp.page_table = page_table; sp.seq_lens = seq_lens; sp.max_pages = max_pages;
-    sp.pool = static_cast<uint8_t*>(const_cast<void*>(pool));
-    sp.ep = make_epi_params(c);
+    sp.step = k_new != nullptr ? 1 : 0;
+    sp.seq_lens = seq_lens;
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, msmem);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg{};

@@ -28,6 +28,8 @@ struct AttnParams {
   float* seg_o;                // [B][H_q][128] unnormalized Σ p v (null: no segment)
   float* seg_m;                // [B][H_q]
   float* seg_l;                // [B][H_q]
+  float* newtok;               // decode step: [B][H_kv][2][128] k̂, v̂ of the new token
+                               // (prologue -> merge)
   int len_adj;                 // decode step: 1 (the partial kernels attend over seq_len - 1
                                // tokens; the merge kernel appends and folds the new token)
   unsigned long long* tl;      // timing probe builds only (-DOSCAR_PROBE_TL): per-CTA/warp

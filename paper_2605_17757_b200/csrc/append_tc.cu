@@ -175,8 +175,11 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
       if (lane == 0) {
         const uint32_t dt = tmem + a * 128;
         const uint32_t abase = su32(S.A[s]), bh = su32(S.Bhi), bl = su32(S.Blo);
+#ifndef OSCAR_PROBE_PARTS
+#define OSCAR_PROBE_PARTS 2      // timing probe only: 1 = the R_hi pass alone (results invalid)
+#endif
 #pragma unroll
-        for (int part = 0; part < 2; ++part) {
+        for (int part = 0; part < OSCAR_PROBE_PARTS; ++part) {
           const uint32_t bbase = part ? bl : bh;
 #pragma unroll
           for (int kc = 0; kc < 2; ++kc)
@@ -292,6 +295,9 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
         continue;
       }
 
+#ifdef OSCAR_PROBE_NOEPI
+      if (v[0] != 0x7fffffffu) continue;           // timing probe only: TMEM drained, nothing stored
+#endif
       const bool valid = slot >= 0;
       // V fast path: the quarter's 32 tokens go to 32 consecutive slots starting on a 16-token
       // tile, i.e. two whole 16-token FORMAT tiles -> stage the FORMAT-ordered bytes in smem and

@@ -504,7 +504,10 @@ __global__ void __launch_bounds__(256) attend_merge_kernel(AttnParams p, const f
   return;                                            // timing probe only (results invalid)
 #endif
   constexpr int WPH = 8 / HC;                        // warps per query head
-  constexpr int NB = 8;                              // splits per load batch (two in flight) per warp
+#ifndef OSCAR_MERGE_NB
+#define OSCAR_MERGE_NB 4      // same-box A/B (C2 decode step): 2 79.9, 4 79.8, 6 81.5, 8 81.0, 16 81.5 us
+#endif
+  constexpr int NB = OSCAR_MERGE_NB;                 // splits per load batch (two in flight) per warp
   constexpr int HPT = (HC + 1) / 2;                  // heads per thread in the un-rotation
   extern __shared__ __align__(128) float Rs[];       // [128][128] R_V[h]
   __shared__ __align__(16) float po[8][kD];

@@ -53,16 +53,17 @@ for l in range(NL):
         lib.oscar_probe_timeline(ctypes.c_void_p(0))
 torch.cuda.synchronize()
 t = tl.cpu().numpy().reshape(3, 8192, 4).astype(np.float64)
-valid = t[0, :, 0] > 0
-t0 = t[0, valid, 0].min()
+marks = t[t > 0]
+t0 = marks.min()                              # earliest mark of any kernel (fused prologue: no kind-0 entry)
 res = {"fn": FN}
 for kind, name, slots in ((0, "prologue", ("entry", "after_wait", "end")), (1, "partial", ("entry", "after_wait", "end")),
                           (2, "merge", ("entry", "pre_wait_done", "after_wait", "end"))):
-    rows = t[kind][t[kind][:, 0] > 0]
+    rows = t[kind][t[kind].max(axis=1) > 0]
     d = {"n": int(rows.shape[0])}
     for i, s in enumerate(slots):
-        x = (rows[:, i] - t0) / 1e3
-        d[s] = [round(float(np.quantile(x, qq)), 2) for qq in (0.0, 0.1, 0.5, 0.9, 1.0)]
+        x = (rows[rows[:, i] > 0, i] - t0) / 1e3
+        if x.size:
+            d[s] = [round(float(np.quantile(x, qq)), 2) for qq in (0.0, 0.1, 0.5, 0.9, 1.0)]
     res[name] = d
 print(json.dumps(res))
 np.save(os.path.join("gpurun_out", f"timeline_{FN}_{os.path.basename(os.environ.get('OSCAR_LIB', 'default'))}.npy"), t)

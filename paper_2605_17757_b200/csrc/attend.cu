@@ -60,7 +60,10 @@ struct PrologueParams {
   const uint16_t* knew;         // decode step: [B][H_kv][128] bf16 new K / V rows (null: attend)
   const uint16_t* vnew;
   const float* RV;              // [H_kv][128][128]; null: pre-rotated V (identity)
-  float* newtok;                // decode step: [B][H_kv][2][128] fp32 k̂, v̂
+  float* newtok;                // decode step: [B][H_kv][kNewTok] fp32 k̂, v̂, logits q̃·k̂ (g)
+  int32_t* nsplit;              // [B] split partials per (sequence, head) of the balanced
+                                // decomposition (attend_mma.cu Decomp), for the merge kernel
+  int balanced, n_warps, pmin, len_adj, P, batch;
   const int32_t* page_table;    // decode step: slot of the new row
   const int32_t* seq_lens;
   int max_pages;
@@ -106,6 +109,27 @@ __global__ void __launch_bounds__(512) attend_prologue_kernel(PrologueParams pp)
   if (threadIdx.x == 0) tl_mark(pp.tl, 0, blockIdx.y * gridDim.x + blockIdx.x, 1);
   const int G = 1 << pp.lgG;
   if (pp.work && b == 0 && h == 0 && tid == 0) *pp.work = 0;   // reset the work-item counter
+  // balanced decomposition: split count of sequence b (warp 15, CTA h = 0; loads overlapping the
+  // rotation), the same formula as the partial kernel's Decomp::rof
+  if (pp.balanced && h == 0 && w == 15) {
+    int lt = 0, tot = 0;
+    for (int bb = lane; bb < pp.batch; bb += 32) {
+      const int n = (max(pp.seq_lens[bb] - pp.len_adj, 0) + pp.P - 1) / pp.P;
+      tot += n;
+      lt += bb < b ? n : 0;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      lt += __shfl_xor_sync(0xffffffffu, lt, o);
+      tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    }
+    if (lane == 0) {
+      const int npg = (max(pp.seq_lens[b] - pp.len_adj, 0) + pp.P - 1) / pp.P;
+      const int64_t T = tot;
+      const int64_t W = min((int64_t)(pp.n_warps / gridDim.y), max((int64_t)1, T / pp.pmin));
+      auto rof = [&](int64_t x) { return ((x + 1) * W - 1) / T; };
+      pp.nsplit[b] = npg > 0 ? (int)(rof(lt + npg - 1) - rof(lt) + 1) : 0;
+    }
+  }
   // decode step: the new row's slot (warps GQ, GQ + 1), its loads overlapping the rotation
   int Lstep = 0;
   int64_t slot = 0;
@@ -172,6 +196,7 @@ __global__ void __launch_bounds__(512) attend_prologue_kernel(PrologueParams pp)
     ys[r][c] = y;
   }
   __syncthreads();
+  if (threadIdx.x == 0) tl_mark(pp.tl, 0, blockIdx.y * gridDim.x + blockIdx.x, 3);
   if (step && (w == GQ || w == GQ + 1)) {
     // QuantizeAndWrite of the new K (warp GQ) / V (warp GQ + 1) row; its dequantized row k̂ / v̂
     // goes to newtok for the merge kernel.  These two warps are done after this: the rest of
@@ -181,8 +206,20 @@ __global__ void __launch_bounds__(512) attend_prologue_kernel(PrologueParams pp)
       const float4 y4 = reinterpret_cast<const float4*>(ys[GQ + isV])[lane];
       float yy[4] = {y4.x, y4.y, y4.z, y4.w}, dq[4];
       quantize_store_row_warp(pp.ep, yy, lane, slot, h, isV, pp.pool, dq);
-      reinterpret_cast<float4*>(pp.newtok + (((size_t)b * gridDim.y + h) * 2 + isV) * kD)[lane] =
-          make_float4(dq[0], dq[1], dq[2], dq[3]);
+      float* nt = pp.newtok + ((size_t)b * gridDim.y + h) * kNewTok;
+      reinterpret_cast<float4*>(nt + isV * kD)[lane] = make_float4(dq[0], dq[1], dq[2], dq[3]);
+      if (!isV) {
+        // the new token's logit (log2 units) per head: q̃·k̂ with q̃ = ys·scale·log₂e as stored
+        // in qt below
+#pragma unroll
+        for (int r = 0; r < GQ; ++r) {
+          const float4 qv = reinterpret_cast<const float4*>(ys[r])[lane];
+          float d = (qv.x * pp.qscale) * dq[0] + (qv.y * pp.qscale) * dq[1] + (qv.z * pp.qscale) * dq[2] +
+                    (qv.w * pp.qscale) * dq[3];
+          for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+          if (lane == 0) nt[2 * kD + r] = d;
+        }
+      }
     }
     return;
   }
@@ -543,43 +580,16 @@ __global__ void __launch_bounds__(256) attend_merge_kernel(AttnParams p, const f
   // from the prologue (newtok)
   const int Lnew = sp.step ? sp.seq_lens[b] : 0;
   if (Lnew > 0) {
-    const float* nt = p.newtok + ((size_t)b * p.hkv + h) * 2 * kD;
+    const float* nt = p.newtok + ((size_t)b * p.hkv + h) * kNewTok;
     if (tid < kD / 4) reinterpret_cast<float4*>(vhat)[tid] = __ldcg(reinterpret_cast<const float4*>(nt + kD) + tid);
-    if (w < HC) {
-      const size_t row = (size_t)b * p.hq + (size_t)h * p.g + hz + w;
-      const float4 qv = __ldcg(reinterpret_cast<const float4*>(p.qt + row * kD) + lane);
-      const float4 kv = __ldcg(reinterpret_cast<const float4*>(nt) + lane);
-      float d = qv.x * kv.x + qv.y * kv.y + qv.z * kv.z + qv.w * kv.w;
-      for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-      if (lane == 0) nlog[w] = d;
-    }
+    if (tid >= 64 && tid < 64 + HC) nlog[tid - 64] = __ldcg(nt + 2 * kD + hz + tid - 64);
   }
   // split partials of this unit: all n_splits slots (simple kernel), or the count of warps whose
-  // range covers the unit under the balanced decomposition (attend_mma.cu, Decomp)
-  int ns = p.n_splits;
-  if (p.balanced) {
-    __shared__ int red[2][8];
-    int lt = 0, tot = 0;
-    for (int bb = tid; bb < p.batch; bb += 256) {
-      const int n = (max(p.seq_lens[bb] - p.len_adj, 0) + p.P - 1) / p.P;
-      tot += n;
-      lt += bb < b ? n : 0;
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-      lt += __shfl_xor_sync(0xffffffffu, lt, o);
-      tot += __shfl_xor_sync(0xffffffffu, tot, o);
-    }
-    if (lane == 0) { red[0][w] = lt; red[1][w] = tot; }
-    __syncthreads();
-    lt = 0; tot = 0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) { lt += red[0][i]; tot += red[1][i]; }
-    const int npg = (max(p.seq_lens[b] - p.len_adj, 0) + p.P - 1) / p.P;
-    const int64_t T = tot;
-    const int64_t W = min((int64_t)(p.n_warps / p.hkv), max((int64_t)1, T / p.pmin));
-    auto rof = [&](int64_t x) { return ((x + 1) * W - 1) / T; };
-    ns = npg > 0 ? (int)(rof(lt + npg - 1) - rof(lt) + 1) : 0;
-  }
+  // range covers the unit under the balanced decomposition (from the prologue)
+  __shared__ int ns_s;
+  if (tid == 96) ns_s = p.balanced ? __ldcg(p.nsplit + b) : p.n_splits;
+  __syncthreads();
+  const int ns = ns_s;
   if (tid == 0) tl_mark(p.tl, 2, tl_idx, 1);
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   if (tid == 0) tl_mark(p.tl, 2, tl_idx, 2);
@@ -809,7 +819,7 @@ static int n_split_slots(const oscar_ctx& c, int B, int max_pages) {
 // Workspace carve-up: every sub-buffer starts on a 256-B boundary (the kernels use 8- and 16-B
 // vector accesses on them, and B·H_q may be odd).
 struct WsLayout {
-  size_t qt, ws_o, ws_m, ws_l, qsum, qscale, qint, qfrag, work, seg_o, seg_m, seg_l, newtok, total;
+  size_t qt, ws_o, ws_m, ws_l, qsum, qscale, qint, qfrag, work, seg_o, seg_m, seg_l, newtok, nsplit, total;
 };
 static WsLayout ws_layout(const oscar_ctx& c, int B, int max_pages) {
   const size_t ns = (size_t)n_split_slots(c, B, max_pages);
@@ -834,7 +844,8 @@ static WsLayout ws_layout(const oscar_ctx& c, int B, int max_pages) {
   w.seg_o = take(rows * kD * 4);
   w.seg_m = take(rows * 4);
   w.seg_l = take(rows * 4);
-  w.newtok = take((size_t)B * c.hkv * 2 * kD * 4);
+  w.newtok = take((size_t)B * c.hkv * kNewTok * 4);
+  w.nsplit = take((size_t)B * 4);
   w.total = off;
   return w;
 }
@@ -888,6 +899,7 @@ cudaError_t launch_attend(const oscar_ctx& c, const void* q, const int32_t* page
     p.qfrag = reinterpret_cast<uint32_t*>(base + w.qfrag);
     p.work = reinterpret_cast<int32_t*>(base + w.work);
     p.newtok = reinterpret_cast<float*>(base + w.newtok);
+    p.nsplit = reinterpret_cast<int32_t*>(base + w.nsplit);
     if (seg_k) {
       p.seg_o = reinterpret_cast<float*>(base + w.seg_o);
       p.seg_m = reinterpret_cast<float*>(base + w.seg_m);
@@ -910,6 +922,8 @@ cudaError_t launch_attend(const oscar_ctx& c, const void* q, const int32_t* page
     pp.tq = mma && attend_mma_tq(c) ? 1 : 0; pp.work = mma ? p.work : nullptr;
     pp.knew = static_cast<const uint16_t*>(k_new); pp.vnew = static_cast<const uint16_t*>(v_new);
     pp.RV = RV; pp.newtok = p.newtok;
+    pp.nsplit = p.nsplit; pp.balanced = p.balanced; pp.n_warps = p.n_warps; pp.pmin = p.pmin;
+    pp.len_adj = k_new != nullptr ? 1 : 0; pp.P = c.P; pp.batch = B;
     pp.page_table = page_table; pp.seq_lens = seq_lens; pp.max_pages = max_pages;
     pp.pool = static_cast<uint8_t*>(const_cast<void*>(pool));
     pp.ep = make_epi_params(c);

@@ -4,6 +4,8 @@
 
 namespace oscar {
 
+constexpr int kNewTok = 2 * 128 + 8;   // floats per (b, h) of the decode step's new-token record
+
 struct AttnParams {
   int hq, hkv, g, P, bits, G, ng;
   int row_bytes, vcodes_off, meta_off, page_bytes;
@@ -28,8 +30,9 @@ struct AttnParams {
   float* seg_o;                // [B][H_q][128] unnormalized Σ p v (null: no segment)
   float* seg_m;                // [B][H_q]
   float* seg_l;                // [B][H_q]
-  float* newtok;               // decode step: [B][H_kv][2][128] k̂, v̂ of the new token
-                               // (prologue -> merge)
+  float* newtok;               // decode step: [B][H_kv][kNewTok] k̂, v̂, logits q̃·k̂ (g) of the
+                               // new token (prologue -> merge)
+  int32_t* nsplit;             // [B] split partials per (sequence, head) (prologue -> merge)
   int len_adj;                 // decode step: 1 (the partial kernels attend over seq_len - 1
                                // tokens; the merge kernel appends and folds the new token)
   unsigned long long* tl;      // timing probe builds only (-DOSCAR_PROBE_TL): per-CTA/warp

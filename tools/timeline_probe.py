@@ -56,7 +56,7 @@ t = tl.cpu().numpy().reshape(3, 8192, 4).astype(np.float64)
 marks = t[t > 0]
 t0 = marks.min()                              # earliest mark of any kernel (fused prologue: no kind-0 entry)
 res = {"fn": FN}
-for kind, name, slots in ((0, "prologue", ("entry", "after_wait", "end")), (1, "partial", ("entry", "after_wait", "end")),
+for kind, name, slots in ((0, "prologue", ("entry", "after_wait", "end", "rotated")), (1, "partial", ("entry", "after_wait", "end")),
                           (2, "merge", ("entry", "pre_wait_done", "after_wait", "end"))):
     rows = t[kind][t[kind].max(axis=1) > 0]
     d = {"n": int(rows.shape[0])}

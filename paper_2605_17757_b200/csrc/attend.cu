@@ -131,15 +131,11 @@ __global__ void __launch_bounds__(512) attend_prologue_kernel(PrologueParams pp)
     }
   }
   // decode step: the new row's slot (warps GQ, GQ + 1), its loads overlapping the rotation
+  // (the length is loaded beside the rows; the dependent page-table load is issued after the
+  // rows have arrived, so its latency overlaps the contraction instead of delaying the barrier)
   int Lstep = 0;
   int64_t slot = 0;
-  if (step && (w == GQ || w == GQ + 1)) {
-    Lstep = pp.seq_lens[b];
-    if (Lstep > 0) {
-      const int pos = Lstep - 1;
-      slot = (int64_t)pp.page_table[(size_t)b * pp.max_pages + pos / pp.ep.P] * pp.ep.P + pos % pp.ep.P;
-    }
-  }
+  if (step && (w == GQ || w == GQ + 1)) Lstep = pp.seq_lens[b];
 #ifdef OSCAR_PROBE_NOPRO
   return;                                            // timing probe only (results invalid)
 #endif
@@ -154,6 +150,10 @@ __global__ void __launch_bounds__(512) attend_prologue_kernel(PrologueParams pp)
                     __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xffff0000u));
   }
   __syncthreads();
+  if (step && (w == GQ || w == GQ + 1) && Lstep > 0) {
+    const int pos = Lstep - 1;
+    slot = (int64_t)pp.page_table[(size_t)b * pp.max_pages + pos / pp.ep.P] * pp.ep.P + pos % pp.ep.P;
+  }
   ptx::mbar_wait(&rbar, 0);                          // R_K (R_V) resident
   // warp w contracts rows 8w..8w+7 of R (lane: columns 4l..4l+3)
   float4 acc[NR];

@@ -36,7 +36,10 @@ constexpr int kStages = 4;
 #ifndef OSCAR_APPEND_ACC
 #define OSCAR_APPEND_ACC 2
 #endif
-constexpr int kAcc = OSCAR_APPEND_ACC;          // TMEM fp32 accumulators (128 columns each)
+#ifndef OSCAR_APPEND_N256
+#define OSCAR_APPEND_N256 1      // C2 prefill (2-bit, G = 64): 0.576 -> 0.549 ms (same-box A/B)
+#endif
+constexpr int kAcc = OSCAR_APPEND_ACC;          // TMEM fp32 accumulators (128 columns each; N256: 256)
 constexpr int kEpiWarps = 16;                   // 4 per TMEM lane quarter: (channel half, tile parity)
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr int kTileBytes = kTok * kD * 2;       // 32 KB bf16 tile
@@ -57,6 +60,10 @@ struct TcSmem {
 using namespace ptx;
 // instruction descriptor: kind::f16, A = B = BF16, D = F32, both K-major, M = 128, N = 128
 constexpr uint32_t kIdesc = idesc_bf16(128, 128, false, false);
+// N256 (MODE 0 / 1): one UMMA 128x256x16 per k-step against B = [R_hi | R_lo] side by side along N
+// (D = [x·R_hi | x·R_lo], the epilogue adds the halves): half the MMA instructions and a quarter
+// less shared-memory operand traffic than two 128x128x16 passes (A is read once per k-step)
+constexpr uint32_t kIdesc256 = idesc_bf16(128, 256, false, false);
 
 struct TcParams {
   const int64_t* slots;
@@ -108,6 +115,9 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
   const int pair = blockIdx.x / p.cpp, sub = blockIdx.x % p.cpp;
   const int h = (MODE == 1 || MODE == 3) ? pair : pair >> 1, isV = (MODE == 1 || MODE == 3) ? 0 : pair & 1;
   const int ntiles = sub < p.tiles_per_pair ? (p.tiles_per_pair - sub + p.cpp - 1) / p.cpp : 0;
+  // (4-bit G = 32, the heaviest epilogue, stays on two N = 128 passes: 0.632 vs 0.640 ms)
+  constexpr bool N256 = OSCAR_APPEND_N256 && MODE != 3 && !(BITS == 4 && G == 32);
+  constexpr int kAccCols = N256 ? 256 : 128;    // TMEM columns per accumulator
 
   // ---- R -> bf16 hi/lo, transposed to K-major (row n = output channel, k contiguous), SW128
   {
@@ -129,16 +139,23 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
         lo[e] = (uint32_t)__bfloat16_as_ushort(l0) | ((uint32_t)__bfloat16_as_ushort(l1) << 16);
       }
       const int kchunk = kc16 >> 3, c16 = kc16 & 7;
-      const int off = kchunk * (kD * 128) + n * 128 + ((c16 ^ (n & 7)) << 4);
-      *reinterpret_cast<uint4*>(S.Bhi + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-      *reinterpret_cast<uint4*>(S.Blo + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+      if (N256) {
+        // [2 k-chunks][256 rows: R_hi columns, then R_lo columns][128 B] across Bhi ‖ Blo
+        const int off = kchunk * (2 * kD * 128) + n * 128 + ((c16 ^ (n & 7)) << 4);
+        *reinterpret_cast<uint4*>(S.Bhi + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+        *reinterpret_cast<uint4*>(S.Bhi + off + kD * 128) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+      } else {
+        const int off = kchunk * (kD * 128) + n * 128 + ((c16 ^ (n & 7)) << 4);
+        *reinterpret_cast<uint4*>(S.Bhi + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+        *reinterpret_cast<uint4*>(S.Blo + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+      }
     }
   }
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) { mbar_init(&S.full[s], 1); mbar_init(&S.empty[s], 1); }
     for (int a = 0; a < kAcc; ++a) { mbar_init(&S.tfull[a], 1); mbar_init(&S.tempty[a], kEpiWarps / 2); }
   }
-  if (warp == 1) tmem_alloc(&S.tmem_base, 128 * kAcc);
+  if (warp == 1) tmem_alloc(&S.tmem_base, kAccCols * kAcc);
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // B writes -> async proxy
   fence_before();
   __syncthreads();
@@ -173,13 +190,21 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
       mbar_wait(&S.full[s], (i / kStages) & 1);
       fence_after();
       if (lane == 0) {
-        const uint32_t dt = tmem + a * 128;
+        const uint32_t dt = tmem + a * kAccCols;
         const uint32_t abase = su32(S.A[s]), bh = su32(S.Bhi), bl = su32(S.Blo);
 #ifndef OSCAR_PROBE_PARTS
 #define OSCAR_PROBE_PARTS 2      // timing probe only: 1 = the R_hi pass alone (results invalid)
 #endif
+        if (N256) {
 #pragma unroll
-        for (int part = 0; part < OSCAR_PROBE_PARTS; ++part) {
+          for (int kc = 0; kc < 2; ++kc)
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              umma_f16<kIdesc256>(dt, kmajor_sw128_desc(abase + kc * (kTileBytes / 2) + kk * 32),
+                                  kmajor_sw128_desc(bh + kc * (2 * kD * 128) + kk * 32), (kc | kk) != 0);
+        }
+#pragma unroll
+        for (int part = 0; part < (N256 ? 0 : OSCAR_PROBE_PARTS); ++part) {
           const uint32_t bbase = part ? bl : bh;
 #pragma unroll
           for (int kc = 0; kc < 2; ++kc)
@@ -224,7 +249,7 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
         // time), then the 64-point transform of this half in registers
         mbar_wait(&S.tfull[a], (i / kAcc) & 1);
         fence_after();
-        const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + a * 128;
+        const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + a * kAccCols;
         float y[64];
 #pragma unroll
         for (int ch = 0; ch < 4; ++ch) {
@@ -264,10 +289,24 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
       if constexpr (MODE != 2) {
         mbar_wait(&S.tfull[a], (i / kAcc) & 1);
         fence_after();
-        const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + a * 128 + half * 64;
-        OSCAR_TMEM_LD32(taddr, v);
-        OSCAR_TMEM_LD32(taddr + 32, (v + 32));
-        tmem_ld_wait();
+        const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + a * kAccCols + half * 64;
+        if (N256) {
+          // x̃ = x·R_hi + x·R_lo: columns c and 128 + c of the accumulator
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            uint32_t lo16[16];
+            OSCAR_TMEM_LD16(taddr + 16 * q4, (v + 16 * q4));
+            OSCAR_TMEM_LD16(taddr + 128 + 16 * q4, lo16);
+            tmem_ld_wait();
+#pragma unroll
+            for (int k = 0; k < 16; ++k)
+              v[16 * q4 + k] = __float_as_uint(__uint_as_float(v[16 * q4 + k]) + __uint_as_float(lo16[k]));
+          }
+        } else {
+          OSCAR_TMEM_LD32(taddr, v);
+          OSCAR_TMEM_LD32(taddr + 32, (v + 32));
+          tmem_ld_wait();
+        }
         fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&S.tempty[a]);
@@ -465,7 +504,7 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
   __syncthreads();
   if (warp == 1) {
     fence_after();
-    tmem_dealloc(tmem, 128 * kAcc);
+    tmem_dealloc(tmem, kAccCols * kAcc);
   }
 }
 

@@ -115,6 +115,9 @@ __device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
 #ifndef OSCAR_APPEND_F2
 #define OSCAR_APPEND_F2 (BITS == 3)
 #endif
+#ifndef OSCAR_APPEND_F2ADD
+#define OSCAR_APPEND_F2ADD OSCAR_APPEND_F2     // the x·R_hi + x·R_lo sum alone as f32x2
+#endif
 
 }  // namespace
 
@@ -325,7 +328,7 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
             OSCAR_TMEM_LD16(taddr + 16 * q4, (v + 16 * q4));
             OSCAR_TMEM_LD16(taddr + 128 + 16 * q4, lo16);
             tmem_ld_wait();
-            if (OSCAR_APPEND_F2) {
+            if (OSCAR_APPEND_F2ADD) {
 #pragma unroll
               for (int k = 0; k < 16; k += 2)
                 unpk2(fadd2(pk2(v[16 * q4 + k], v[16 * q4 + k + 1]), pk2(lo16[k], lo16[k + 1])), v[16 * q4 + k],

@@ -166,6 +166,9 @@ oscar_status oscar_calib_sv(const oscar_ctx* ctx, const void* Q, const void* K, 
   if (N == 0) return OSCAR_OK;
   if (n_seq < 1) return fail(OSCAR_ERR_ARG, "n_seq must be >= 1");
   if (!Q || !K || !V || !seq_starts || !SV) return fail(OSCAR_ERR_ARG, "oscar_calib_sv: NULL pointer");
+  if (ctx->variant == 0 && oscar::calib_sv_tc_supported(*ctx) && aligned16(Q) && aligned16(K) && aligned16(V))
+    return cuda_status(oscar::launch_calib_sv_tc(*ctx, Q, K, V, seq_starts, n_seq, N, SV, as_stream(stream)),
+                       "calib_sv_tc");
   return cuda_status(oscar::launch_calib_sv(*ctx, Q, K, V, seq_starts, n_seq, N, SV, as_stream(stream)), "calib_sv");
 }
 

@@ -1,0 +1,299 @@
+// On-device S·V for the C_S target on the 5th-generation tensor cores (variant 0; SURVEY §8(f)
+// NEXT-3; Alg. 1 `Calibrate` P:L1604-1606: S = softmax(Q Kᵀ/√d + M), C_S from S·V).
+// Reading Z16: M is causal including the diagonal and block-diagonal across the calibration
+// sequences; query head i uses KV head i/g.  Same result as calib_sv.cu (the mma.sync kernel,
+// variant 1) up to fp32 summation order: P is rounded to bf16 before the P·V product in both.
+//
+// One CTA = 128 queries of one query head, 6 warps:
+//   warp 4  TMA producer: the Q tile once, then 128-key K and V tiles (two 64-channel SWIZZLE_128B
+//           boxes each) into a 2-stage ring
+//   warp 5  TMEM allocator + single-thread tcgen05.mma issuer:
+//             S_j  = Q·K_jᵀ      (A = Q K-major, B = K_j K-major)   -> TMEM columns 128·(j % 2)
+//             O   += P_j·V_j     (A = P_j K-major from smem, B = V_j MN-major) -> TMEM columns 256..383
+//   warps 0-3  softmax (thread = query row = TMEM lane): per key block, pass 1 reads S and forms
+//           the masked row max; the running max m moves only when the block max exceeds it by more
+//           than 2^8 (then O is rescaled in TMEM by exp2(m_old - m_new)), otherwise P ≤ 2^8 stays
+//           exact in range for bf16; pass 2 writes P = exp2(S·scale·log2e - m) as bf16 into the
+//           swizzled K-major smem tile the next P·V reads, and sums l.  At the end O / l -> SV bf16.
+#include "common.cuh"
+#include "ptx.cuh"
+
+namespace oscar {
+
+namespace {
+using namespace ptx;
+
+constexpr int kSvQ = 128;                     // queries per CTA (UMMA M)
+constexpr int kSvK = 128;                     // keys per block
+constexpr int kSvHalf = 128 * 128;            // one 64-channel (or 64-key) half tile: 128 rows x 128 B
+constexpr int kSvThreads = 6 * 32;
+constexpr float kRescaleThr = 8.f;            // log2 units
+
+struct SvSmem {
+  alignas(1024) uint8_t Q[2][kSvHalf];        // [channel half][query row][128 B]
+  alignas(1024) uint8_t K[2][2][kSvHalf];     // [stage][channel half][key row][128 B]
+  alignas(1024) uint8_t V[2][2][kSvHalf];     // [stage][channel half][key row][128 B]
+  alignas(1024) uint8_t P[2][kSvHalf];        // [key half][query row][128 B] (bf16 P, SW128)
+  uint64_t qfull, kvfull[2], kvempty[2], sfull[2], sempty[2], pfull, pvfull;
+  uint32_t tmem_base;
+};
+
+constexpr uint32_t kIdescS = idesc_bf16(128, 128, false, false);   // A, B K-major
+constexpr uint32_t kIdescPV = idesc_bf16(128, 128, false, true);   // B (V) MN-major
+
+#define OSCAR_TMEM_ST32(base, v)                                                                     \
+  asm volatile(                                                                                       \
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"  \
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};\n"                   \
+      ::"r"(base), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]),        \
+        "r"(v[7]), "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]),   \
+        "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]),            \
+        "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]),            \
+        "r"(v[29]), "r"(v[30]), "r"(v[31])                                                             \
+      : "memory")
+
+// sequence containing token n: the last s with starts[s] <= n
+__device__ __forceinline__ int sv_seq_start(const int32_t* starts, int n_seq, int n) {
+  int lo = 0, hi = n_seq - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (starts[mid] <= n) lo = mid; else hi = mid - 1;
+  }
+  return starts[lo];
+}
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;\n" : "=f"(y) : "f"(x));
+  return y;
+}
+
+struct SvParams {
+  const int32_t* starts;
+  int n_seq, N, hq, hkv, nqb;
+  float scale_log2;
+  uint16_t* SV;
+};
+}  // namespace
+
+__global__ void __launch_bounds__(kSvThreads, 1)
+calib_sv_tc_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapK,
+                   const __grid_constant__ CUtensorMap mapV, SvParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  SvSmem& S = *reinterpret_cast<SvSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qb = p.nqb - 1 - (int)blockIdx.x;          // longest key ranges first
+  const int qh = blockIdx.y, h = qh / (p.hq / p.hkv);
+  const int q0 = qb * kSvQ;
+  const int qlast = min(q0 + kSvQ, p.N) - 1;
+  const int kbeg = sv_seq_start(p.starts, p.n_seq, q0);
+  const int nblk = (qlast - kbeg) / kSvK + 1;
+
+  if (threadIdx.x == 0) {
+    mbar_init(&S.qfull, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&S.kvfull[s], 1); mbar_init(&S.kvempty[s], 1);
+      mbar_init(&S.sfull[s], 1); mbar_init(&S.sempty[s], 4);
+    }
+    mbar_init(&S.pfull, 4);
+    mbar_init(&S.pvfull, 1);
+    mbar_init_fence();
+  }
+  if (warp == 5) tmem_alloc(&S.tmem_base, 512);
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = S.tmem_base;
+
+  if (warp == 4) {
+    // ================= TMA producer
+    if (lane == 0) {
+      mbar_expect_tx(&S.qfull, 2 * kSvHalf);
+      tma_load_3d(S.Q[0], &mapQ, 0, qh, q0, &S.qfull);
+      tma_load_3d(S.Q[1], &mapQ, 64, qh, q0, &S.qfull);
+      for (int j = 0; j < nblk; ++j) {
+        const int s = j & 1, key0 = kbeg + j * kSvK;
+        mbar_wait(&S.kvempty[s], ((j >> 1) & 1) ^ 1);
+        mbar_expect_tx(&S.kvfull[s], 4 * kSvHalf);
+        tma_load_3d(S.K[s][0], &mapK, 0, h, key0, &S.kvfull[s]);
+        tma_load_3d(S.K[s][1], &mapK, 64, h, key0, &S.kvfull[s]);
+        tma_load_3d(S.V[s][0], &mapV, 0, h, key0, &S.kvfull[s]);
+        tma_load_3d(S.V[s][1], &mapV, 64, h, key0, &S.kvfull[s]);
+      }
+    }
+  } else if (warp == 5) {
+    // ================= MMA issuer: S_j, then P_{j-1}·V_{j-1}
+    mbar_wait(&S.qfull, 0);
+    for (int j = 0; j <= nblk; ++j) {
+      if (j < nblk) {
+        const int s = j & 1;
+        mbar_wait(&S.kvfull[s], (j >> 1) & 1);
+        mbar_wait(&S.sempty[s], ((j >> 1) & 1) ^ 1);
+        fence_after();
+        if (lane == 0) {
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            umma_f16<kIdescS>(tmem + 128 * s, kmajor_sw128_desc(su32(S.Q[kk >> 2]) + (kk & 3) * 32),
+                              kmajor_sw128_desc(su32(S.K[s][kk >> 2]) + (kk & 3) * 32), kk != 0);
+          umma_commit(&S.sfull[s]);
+        }
+        __syncwarp();
+      }
+      if (j >= 1) {
+        const int jj = j - 1, s = jj & 1;
+        mbar_wait(&S.pfull, jj & 1);
+        fence_after();
+        if (lane == 0) {
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            umma_f16<kIdescPV>(tmem + 256, kmajor_sw128_desc(su32(S.P[kk >> 2]) + (kk & 3) * 32),
+                               mnmajor_sw128_desc(su32(S.V[s][0]) + kk * 2048, kSvHalf), (jj | kk) != 0);
+          umma_commit(&S.kvempty[s]);     // K_jj, V_jj consumed
+          umma_commit(&S.pvfull);         // O holds blocks 0..jj; P free
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // ================= softmax: thread = query row r (TMEM lane quarter = warp)
+    const int r = warp * 32 + lane;
+    const int qi = q0 + r;
+    const bool live = qi < p.N;
+    const int lo = live ? sv_seq_start(p.starts, p.n_seq, qi) : 0x7fffffff;
+    const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < nblk; ++j) {
+      const int b = j & 1, key0 = kbeg + j * kSvK;
+      mbar_wait(&S.sfull[b], (j >> 1) & 1);
+      fence_after();
+      // keys key0 + c valid for this row: lo <= key <= qi
+      const int cmin = lo - key0, cmax = live ? qi - key0 : -1;
+      // pass 1: masked block max (log2 units)
+      float bm = -INFINITY;
+#pragma unroll 1
+      for (int c0 = 0; c0 < kSvK; c0 += 32) {
+        uint32_t v[32];
+        OSCAR_TMEM_LD32(trow + 128 * b + c0, v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const int c = c0 + k;
+          if (c >= cmin && c <= cmax) bm = fmaxf(bm, __uint_as_float(v[k]) * p.scale_log2);
+        }
+      }
+      // P_{j-1}·V_{j-1} done: O may be rescaled and the P tile rewritten
+      if (j >= 1) {
+        mbar_wait(&S.pvfull, (j - 1) & 1);
+        fence_after();
+      }
+      // (the TMEM load / store below are warp-collective: the rescale runs for the whole warp,
+      // lanes that keep their max multiply by 1)
+      const bool upd = bm > m + kRescaleThr || (m == -INFINITY && bm > -INFINITY);
+      const bool resc = upd && m != -INFINITY;
+      float a = 1.f;
+      if (resc) { a = ex2(m - bm); l *= a; }
+      if (upd) m = bm;
+      if (__any_sync(0xffffffffu, resc)) {
+#pragma unroll 1
+        for (int c0 = 0; c0 < kD; c0 += 32) {
+          uint32_t o[32];
+          OSCAR_TMEM_LD32(trow + 256 + c0, o);
+          tmem_ld_wait();
+#pragma unroll
+          for (int k = 0; k < 32; ++k) o[k] = __float_as_uint(__uint_as_float(o[k]) * a);
+          OSCAR_TMEM_ST32(trow + 256 + c0, o);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+      }
+      // pass 2: P = exp2(s·scale - m) (0 where masked) as bf16 into P[key half][row r]
+#pragma unroll 1
+      for (int c0 = 0; c0 < kSvK; c0 += 32) {
+        uint32_t v[32];
+        OSCAR_TMEM_LD32(trow + 128 * b + c0, v);
+        tmem_ld_wait();
+        uint32_t pk[16];
+#pragma unroll
+        for (int k = 0; k < 32; k += 2) {
+          const int c = c0 + k;
+          const float p0 = (c >= cmin && c <= cmax) ? ex2(__uint_as_float(v[k]) * p.scale_log2 - m) : 0.f;
+          const float p1 = (c + 1 >= cmin && c + 1 <= cmax) ? ex2(__uint_as_float(v[k + 1]) * p.scale_log2 - m) : 0.f;
+          l += p0 + p1;
+          pk[k >> 1] = pack_bf16x2(p0, p1);
+        }
+        // keys c0 .. c0 + 31 = 16-B chunks c0/8 .. c0/8 + 3 of key half c0 / 64
+        uint8_t* base = S.P[c0 >> 6] + r * 128;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int c16 = ((c0 & 63) >> 3) + q;
+          *reinterpret_cast<uint4*>(base + ((c16 ^ (r & 7)) << 4)) =
+              make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // P -> the MMA's async proxy
+      fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&S.sempty[b]);
+        mbar_arrive(&S.pfull);
+      }
+    }
+    // O / l -> SV bf16 [N][H_q][128]
+    mbar_wait(&S.pvfull, (nblk - 1) & 1);
+    fence_after();
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    uint16_t* dst = p.SV + ((size_t)qi * p.hq + qh) * kD;
+#pragma unroll 1
+    for (int c0 = 0; c0 < kD; c0 += 32) {
+      uint32_t o[32];
+      OSCAR_TMEM_LD32(trow + 256 + c0, o);
+      tmem_ld_wait();
+      if (live) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          reinterpret_cast<uint4*>(dst + c0)[q] = make_uint4(
+              pack_bf16x2(__uint_as_float(o[8 * q]) * inv, __uint_as_float(o[8 * q + 1]) * inv),
+              pack_bf16x2(__uint_as_float(o[8 * q + 2]) * inv, __uint_as_float(o[8 * q + 3]) * inv),
+              pack_bf16x2(__uint_as_float(o[8 * q + 4]) * inv, __uint_as_float(o[8 * q + 5]) * inv),
+              pack_bf16x2(__uint_as_float(o[8 * q + 6]) * inv, __uint_as_float(o[8 * q + 7]) * inv));
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 5) {
+    fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ---------------------------------------------------------------- host side
+bool calib_sv_tc_supported(const oscar_ctx& c) {
+  return c.d == 128 && ptx::encode_tiled_fn() != nullptr;
+}
+
+cudaError_t launch_calib_sv_tc(const oscar_ctx& c, const void* Q, const void* K, const void* V,
+                               const int32_t* starts, int n_seq, int64_t N, void* SV, cudaStream_t s) {
+  if ((reinterpret_cast<uintptr_t>(Q) | reinterpret_cast<uintptr_t>(K) | reinterpret_cast<uintptr_t>(V)) & 15)
+    return cudaErrorMisalignedAddress;
+  CUtensorMap mq, mk, mv;
+  if (!ptx::make_bf16_map_3d(&mq, Q, N, c.hq, 1, kSvQ) || !ptx::make_bf16_map_3d(&mk, K, N, c.hkv, 1, kSvK) ||
+      !ptx::make_bf16_map_3d(&mv, V, N, c.hkv, 1, kSvK))
+    return cudaErrorInvalidValue;
+  SvParams p{};
+  p.starts = starts; p.n_seq = n_seq; p.N = (int)N; p.hq = c.hq; p.hkv = c.hkv;
+  p.nqb = (int)((N + kSvQ - 1) / kSvQ);
+  p.scale_log2 = c.scale * kLog2e;
+  p.SV = static_cast<uint16_t*>(SV);
+  const int smem = (int)sizeof(SvSmem) + 1024;
+  cudaError_t e = cudaFuncSetAttribute(calib_sv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  calib_sv_tc_kernel<<<dim3((unsigned)p.nqb, (unsigned)c.hq), kSvThreads, smem, s>>>(mq, mk, mv, p);
+  return cudaGetLastError();
+}
+
+}  // namespace oscar

@@ -31,6 +31,10 @@ cudaError_t launch_cov_accum(const oscar_ctx& c, const void* Q, const void* SV, 
 // calib_sv.cu (S·V for C_S on device, NEXT-3)
 cudaError_t launch_calib_sv(const oscar_ctx& c, const void* Q, const void* K, const void* V,
                             const int32_t* starts, int n_seq, int64_t N, void* SV, cudaStream_t s);
+// calib_sv_tc.cu (the same on tcgen05, variant 0)
+bool calib_sv_tc_supported(const oscar_ctx& c);
+cudaError_t launch_calib_sv_tc(const oscar_ctx& c, const void* Q, const void* K, const void* V,
+                               const int32_t* starts, int n_seq, int64_t N, void* SV, cudaStream_t s);
 // clip.cu (CalibrateClip surrogate objectives, reading Z34)
 constexpr int kMaxClipGrid = 16;
 cudaError_t launch_calib_clip(const oscar_ctx& c, const void* K, const void* V, int64_t N,

@@ -18,8 +18,10 @@ def T(x, dtype=None):
     return t.to(dtype) if dtype is not None else t
 
 
-@pytest.mark.parametrize("seq_lens,Hq,Hkv", [([300, 1, 77, 200], 8, 2), ([64], 4, 4), ([130, 260], 16, 2)])
-def test_calib_sv_parity(seq_lens, Hq, Hkv):
+@pytest.mark.parametrize("seq_lens,Hq,Hkv", [([300, 1, 77, 200], 8, 2), ([64], 4, 4), ([130, 260], 16, 2),
+                                             ([1000, 129, 384], 8, 2)])
+@pytest.mark.parametrize("variant", [0, 1])     # 0: tcgen05 kernel, 1: mma.sync kernel
+def test_calib_sv_parity(seq_lens, Hq, Hkv, variant):
     import torch
     from paper_2605_17757_b200 import binding as B
     rng = np.random.default_rng(sum(seq_lens) + Hq)
@@ -30,6 +32,7 @@ def test_calib_sv_parity(seq_lens, Hq, Hkv):
     ref = O.score_value(Q, K, V, seq_lens)
     starts = np.concatenate([[0], np.cumsum(seq_lens)[:-1]]).astype(np.int32)
     o = B.Oscar(B.Config(num_q_heads=Hq, num_kv_heads=Hkv))
+    o.set_variant(variant)
     sv = torch.empty((N, Hq, 128), dtype=torch.bfloat16, device="cuda")
     o.calib_sv(T(Q, torch.bfloat16), T(K, torch.bfloat16), T(V, torch.bfloat16), T(starts), sv)
     got = sv.float().cpu().numpy()

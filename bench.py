@@ -42,6 +42,15 @@ def measured_peaks():
         return 6650.0, 1400.0, "fallback"
 
 
+def bf16_burst_peak():
+    """Dense bf16 TFLOP/s of a kernel timed alone: MEASURED_PEAKS.json's burst figure."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["bf16_tflops"]), "measured (burst)"
+    except Exception:
+        return 2250.0, "nominal (no MEASURED_PEAKS.json)"
+
+
 # ------------------------------------------------------------------ clocks sampler (NVML)
 class ClockSampler:
     REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
@@ -555,6 +564,10 @@ def main():
             "finalize_ms": t_fin, "jacobi_sweeps_max": int(sweeps.max()),
             "sv_ms_per_layer": t_sv, "sv_TFLOPs": sv_flops / t_sv / 1e9,
             "sv_config": f"causal S·V, {calib_tokens // 8192} sequences x 8192 tokens, {HQ} q-heads",
+            "sv_roofline": {"bound": "tensor", "achieved": sv_flops / t_sv / 1e9, "peak": bf16_burst_peak()[0],
+                            "unit": "TFLOP/s", "frac": sv_flops / t_sv / 1e9 / bf16_burst_peak()[0],
+                            "traffic": None, "kernel": "calib_sv_tc_kernel (tcgen05 + TMA), one layer",
+                            "algorithmic_flops_per_launch": sv_flops, "peak_kind": bf16_burst_peak()[1]},
             "clip_ms_per_layer": t_clip, "clip_config": "8192 rows x 8 kv heads x K,V x 5 ratios",
             "clip_choice_layer0": [rho_k, rho_v],
             "roofline": {"bound": "hbm", "achieved": cov_bytes / t_acc / 1e6, "peak": hbm_peak, "unit": "GB/s",

@@ -566,7 +566,8 @@ def main():
             "sv_config": f"causal S·V, {calib_tokens // 8192} sequences x 8192 tokens, {HQ} q-heads",
             "sv_roofline": {"bound": "tensor", "achieved": sv_flops / t_sv / 1e9, "peak": bf16_burst_peak()[0],
                             "unit": "TFLOP/s", "frac": sv_flops / t_sv / 1e9 / bf16_burst_peak()[0],
-                            "traffic": None, "kernel": "calib_sv_tc_kernel (tcgen05 + TMA), one layer",
+                            "traffic": ncu_traffic(["calib_sv_tc_kernel"]),
+                            "kernel": "calib_sv_tc_kernel (tcgen05 + TMA), one layer",
                             "algorithmic_flops_per_launch": sv_flops, "peak_kind": bf16_burst_peak()[1]},
             "clip_ms_per_layer": t_clip, "clip_config": "8192 rows x 8 kv heads x K,V x 5 ratios",
             "clip_choice_layer0": [rho_k, rho_v],

@@ -95,10 +95,15 @@ __global__ void __launch_bounds__(512) attend_prologue_kernel(PrologueParams pp)
     constexpr uint32_t bytes = kD * kD * 4;
     ptx::mbar_init(&rbar, 1);
     ptx::mbar_init_fence();
+#ifdef OSCAR_PROBE_NOR
+    ptx::mbar_arrive(&rbar);                         // timing probe only: R not loaded (results invalid)
+    if (false)
+#else
     ptx::mbar_expect_tx(&rbar, rotv ? 2 * bytes : bytes);
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
                  ::"r"(ptx::su32(Rks)), "l"(pp.RK + (size_t)h * kD * kD), "r"(bytes), "r"(ptx::su32(&rbar)) : "memory");
     if (rotv)
+#endif
       asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
                    ::"r"(ptx::su32(Rvs)), "l"(pp.RV + (size_t)h * kD * kD), "r"(bytes), "r"(ptx::su32(&rbar)) : "memory");
   }
@@ -517,7 +522,7 @@ __global__ void __launch_bounds__(128) attend_partial_simple(AttnParams p) {
 // (partial row float4 = channels 4l..4l+3, split max and sum) and folds them with a running max;
 // the 8/g warps of a head and the NEXT-1 segment are combined through smem.  Un-rotation:
 // thread (c', half) forms output channel c' of every other head from smem, the contraction index
-// rotated by lane (c = 4·((k + lane) mod 32)) so the 32 rows of a warp hit distinct banks.
+// rotated by lane % 8 (c = 4·((k + lane mod 8) mod 32)): conflict-free R_V rows, broadcast õ.
 //
 // Decode step (Alg. 1 DecodeStep; reading Z35): the prologue has stored the step's
 // new K/V row (QuantizeAndWrite) and left its dequantized rows k̂, v̂ in the workspace (newtok);
@@ -686,7 +691,10 @@ __global__ void __launch_bounds__(256) attend_merge_kernel(AttnParams p, const f
     const float4* Rrow = reinterpret_cast<const float4*>(Rs + (size_t)cp * kD);
 #pragma unroll 8
     for (int k = 0; k < kD / 4; ++k) {
-      const int c4 = (k + lane) & 31;
+      // contraction chunk rotated by lane % 8: the 8 chunk positions cover the 32 banks, so the
+      // R_V row reads are conflict-free (4 wavefronts per warp, the minimum for 512 B) and the
+      // õ reads touch 8 distinct chunks (1 wavefront, broadcast)
+      const int c4 = (k + (lane & 7)) & 31;
       const float4 r = Rrow[c4];
 #pragma unroll
       for (int j = 0; j < HPT; ++j) {

@@ -173,17 +173,27 @@ calib_sv_tc_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_consta
       fence_after();
       // keys key0 + c valid for this row: lo <= key <= qi
       const int cmin = lo - key0, cmax = live ? qi - key0 : -1;
-      // pass 1: masked block max (log2 units)
+      // a block every key of which every row of the warp may see (the usual case below the
+      // diagonal) takes the unmasked loops
+      const bool full = __all_sync(0xffffffffu, cmin <= 0 && cmax >= kSvK - 1);
+      // pass 1: masked block max (log2 units; scale > 0, so max(s)·scale = max(s·scale))
       float bm = -INFINITY;
 #pragma unroll 1
       for (int c0 = 0; c0 < kSvK; c0 += 32) {
         uint32_t v[32];
         OSCAR_TMEM_LD32(trow + 128 * b + c0, v);
         tmem_ld_wait();
+        if (full) {
+          float x = __uint_as_float(v[0]);
 #pragma unroll
-        for (int k = 0; k < 32; ++k) {
-          const int c = c0 + k;
-          if (c >= cmin && c <= cmax) bm = fmaxf(bm, __uint_as_float(v[k]) * p.scale_log2);
+          for (int k = 1; k < 32; ++k) x = fmaxf(x, __uint_as_float(v[k]));
+          bm = fmaxf(bm, x * p.scale_log2);
+        } else {
+#pragma unroll
+          for (int k = 0; k < 32; ++k) {
+            const int c = c0 + k;
+            if (c >= cmin && c <= cmax) bm = fmaxf(bm, __uint_as_float(v[k]) * p.scale_log2);
+          }
         }
       }
       // P_{j-1}·V_{j-1} done: O may be rescaled and the P tile rewritten
@@ -217,13 +227,25 @@ calib_sv_tc_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_consta
         OSCAR_TMEM_LD32(trow + 128 * b + c0, v);
         tmem_ld_wait();
         uint32_t pk[16];
+        if (full) {
+          float l0 = 0.f, l1 = 0.f;
 #pragma unroll
-        for (int k = 0; k < 32; k += 2) {
-          const int c = c0 + k;
-          const float p0 = (c >= cmin && c <= cmax) ? ex2(__uint_as_float(v[k]) * p.scale_log2 - m) : 0.f;
-          const float p1 = (c + 1 >= cmin && c + 1 <= cmax) ? ex2(__uint_as_float(v[k + 1]) * p.scale_log2 - m) : 0.f;
-          l += p0 + p1;
-          pk[k >> 1] = pack_bf16x2(p0, p1);
+          for (int k = 0; k < 32; k += 2) {
+            const float p0 = ex2(fmaf(__uint_as_float(v[k]), p.scale_log2, -m));
+            const float p1 = ex2(fmaf(__uint_as_float(v[k + 1]), p.scale_log2, -m));
+            l0 += p0; l1 += p1;
+            pk[k >> 1] = pack_bf16x2(p0, p1);
+          }
+          l += l0 + l1;
+        } else {
+#pragma unroll
+          for (int k = 0; k < 32; k += 2) {
+            const int c = c0 + k;
+            const float p0 = (c >= cmin && c <= cmax) ? ex2(__uint_as_float(v[k]) * p.scale_log2 - m) : 0.f;
+            const float p1 = (c + 1 >= cmin && c + 1 <= cmax) ? ex2(__uint_as_float(v[k + 1]) * p.scale_log2 - m) : 0.f;
+            l += p0 + p1;
+            pk[k >> 1] = pack_bf16x2(p0, p1);
+          }
         }
         // keys c0 .. c0 + 31 = 16-B chunks c0/8 .. c0/8 + 3 of key half c0 / 64
         uint8_t* base = S.P[c0 >> 6] + r * 128;

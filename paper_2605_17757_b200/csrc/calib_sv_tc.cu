@@ -4,13 +4,14 @@
 // sequences; query head i uses KV head i/g.  Same result as calib_sv.cu (the mma.sync kernel,
 // variant 1) up to fp32 summation order: P is rounded to bf16 before the P·V product in both.
 //
-// One CTA = 128 queries of one query head, 6 warps:
-//   warp 4  TMA producer: the Q tile once, then 128-key K and V tiles (two 64-channel SWIZZLE_128B
+// One CTA = 128 queries of one query head, 10 warps:
+//   warp 8  TMA producer: the Q tile once, then 128-key K and V tiles (two 64-channel SWIZZLE_128B
 //           boxes each) into a 2-stage ring
-//   warp 5  TMEM allocator + single-thread tcgen05.mma issuer:
+//   warp 9  TMEM allocator + single-thread tcgen05.mma issuer:
 //             S_j  = Q·K_jᵀ      (A = Q K-major, B = K_j K-major)   -> TMEM columns 128·(j % 2)
 //             O   += P_j·V_j     (A = P_j K-major from smem, B = V_j MN-major) -> TMEM columns 256..383
-//   warps 0-3  softmax (thread = query row = TMEM lane): per key block, pass 1 reads S and forms
+//   warps 0-7  softmax (thread = query row = TMEM lane; warps q and q + 4 take key columns 0-63 /
+//           64-127 of the rows of lane quarter q, combining max and sum through smem): per key block, pass 1 reads S and forms
 //           the masked row max; the running max m moves only when the block max exceeds it by more
 //           than 2^8 (then O is rescaled in TMEM by exp2(m_old - m_new)), otherwise P ≤ 2^8 stays
 //           exact in range for bf16; pass 2 writes P = exp2(S·scale·log2e - m) as bf16 into the
@@ -26,7 +27,7 @@ using namespace ptx;
 constexpr int kSvQ = 128;                     // queries per CTA (UMMA M)
 constexpr int kSvK = 128;                     // keys per block
 constexpr int kSvHalf = 128 * 128;            // one 64-channel (or 64-key) half tile: 128 rows x 128 B
-constexpr int kSvThreads = 6 * 32;
+constexpr int kSvThreads = 10 * 32;
 constexpr float kRescaleThr = 8.f;            // log2 units
 
 struct SvSmem {
@@ -36,6 +37,8 @@ struct SvSmem {
   alignas(1024) uint8_t P[2][kSvHalf];        // [key half][query row][128 B] (bf16 P, SW128)
   uint64_t qfull, kvfull[2], kvempty[2], sfull[2], sempty[2], pfull, pvfull;
   uint32_t tmem_base;
+  float xmax[2][2][128];                      // [block parity][column half][row] softmax max exchange
+  float xl[2][128];                           // [column half][row] final row sums
 };
 
 constexpr uint32_t kIdescS = idesc_bf16(128, 128, false, false);   // A, B K-major
@@ -98,19 +101,19 @@ calib_sv_tc_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_consta
     mbar_init(&S.qfull, 1);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&S.kvfull[s], 1); mbar_init(&S.kvempty[s], 1);
-      mbar_init(&S.sfull[s], 1); mbar_init(&S.sempty[s], 4);
+      mbar_init(&S.sfull[s], 1); mbar_init(&S.sempty[s], 8);
     }
-    mbar_init(&S.pfull, 4);
+    mbar_init(&S.pfull, 8);
     mbar_init(&S.pvfull, 1);
     mbar_init_fence();
   }
-  if (warp == 5) tmem_alloc(&S.tmem_base, 512);
+  if (warp == 9) tmem_alloc(&S.tmem_base, 512);
   fence_before();
   __syncthreads();
   fence_after();
   const uint32_t tmem = S.tmem_base;
 
-  if (warp == 4) {
+  if (warp == 8) {
     // ================= TMA producer
     if (lane == 0) {
       mbar_expect_tx(&S.qfull, 2 * kSvHalf);
@@ -126,7 +129,7 @@ calib_sv_tc_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_consta
         tma_load_3d(S.V[s][1], &mapV, 64, h, key0, &S.kvfull[s]);
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == 9) {
     // ================= MMA issuer: S_j, then P_{j-1}·V_{j-1}
     mbar_wait(&S.qfull, 0);
     for (int j = 0; j <= nblk; ++j) {
@@ -160,12 +163,16 @@ calib_sv_tc_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_consta
       }
     }
   } else {
-    // ================= softmax: thread = query row r (TMEM lane quarter = warp)
-    const int r = warp * 32 + lane;
+    // ================= softmax: thread = query row r, key / channel columns [64·ch, 64·ch + 64)
+    // (two warps per TMEM lane quarter: warps q and q + 4 split the row's columns; the row max and
+    // the row sum are combined through shared memory, named barrier 1 + q)
+    const int quarter = warp & 3, ch = warp >> 2;
+    const int r = quarter * 32 + lane;
     const int qi = q0 + r;
     const bool live = qi < p.N;
     const int lo = live ? sv_seq_start(p.starts, p.n_seq, qi) : 0x7fffffff;
-    const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+    const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16);
+    const int cb = 64 * ch;                          // first column of this warp
     float m = -INFINITY, l = 0.f;
     for (int j = 0; j < nblk; ++j) {
       const int b = j & 1, key0 = kbeg + j * kSvK;
@@ -173,13 +180,13 @@ calib_sv_tc_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_consta
       fence_after();
       // keys key0 + c valid for this row: lo <= key <= qi
       const int cmin = lo - key0, cmax = live ? qi - key0 : -1;
-      // a block every key of which every row of the warp may see (the usual case below the
-      // diagonal) takes the unmasked loops
-      const bool full = __all_sync(0xffffffffu, cmin <= 0 && cmax >= kSvK - 1);
-      // pass 1: masked block max (log2 units; scale > 0, so max(s)·scale = max(s·scale))
+      // columns every row of the warp may see in full (the usual case below the diagonal) take the
+      // unmasked loops
+      const bool full = __all_sync(0xffffffffu, cmin <= cb && cmax >= cb + 63);
+      // pass 1: masked max of this half (log2 units; scale > 0, so max(s)·scale = max(s·scale))
       float bm = -INFINITY;
 #pragma unroll 1
-      for (int c0 = 0; c0 < kSvK; c0 += 32) {
+      for (int c0 = cb; c0 < cb + 64; c0 += 32) {
         uint32_t v[32];
         OSCAR_TMEM_LD32(trow + 128 * b + c0, v);
         tmem_ld_wait();
@@ -196,13 +203,17 @@ calib_sv_tc_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_consta
           }
         }
       }
+      S.xmax[b][ch][r] = bm;
+      asm volatile("bar.sync %0, 64;\n" ::"r"(1 + quarter) : "memory");
+      bm = fmaxf(bm, S.xmax[b][ch ^ 1][r]);
       // P_{j-1}·V_{j-1} done: O may be rescaled and the P tile rewritten
       if (j >= 1) {
         mbar_wait(&S.pvfull, (j - 1) & 1);
         fence_after();
       }
-      // (the TMEM load / store below are warp-collective: the rescale runs for the whole warp,
-      // lanes that keep their max multiply by 1)
+      // (both warps of the row take the same decision; the TMEM load / store below are
+      // warp-collective: the rescale runs for the whole warp, lanes that keep their max multiply
+      // by 1)
       const bool upd = bm > m + kRescaleThr || (m == -INFINITY && bm > -INFINITY);
       const bool resc = upd && m != -INFINITY;
       float a = 1.f;
@@ -210,7 +221,7 @@ calib_sv_tc_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_consta
       if (upd) m = bm;
       if (__any_sync(0xffffffffu, resc)) {
 #pragma unroll 1
-        for (int c0 = 0; c0 < kD; c0 += 32) {
+        for (int c0 = cb; c0 < cb + 64; c0 += 32) {
           uint32_t o[32];
           OSCAR_TMEM_LD32(trow + 256 + c0, o);
           tmem_ld_wait();
@@ -220,9 +231,9 @@ calib_sv_tc_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_consta
         }
         asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
       }
-      // pass 2: P = exp2(s·scale - m) (0 where masked) as bf16 into P[key half][row r]
+      // pass 2: P = exp2(s·scale - m) (0 where masked) as bf16 into P[key half ch][row r]
 #pragma unroll 1
-      for (int c0 = 0; c0 < kSvK; c0 += 32) {
+      for (int c0 = cb; c0 < cb + 64; c0 += 32) {
         uint32_t v[32];
         OSCAR_TMEM_LD32(trow + 128 * b + c0, v);
         tmem_ld_wait();
@@ -247,8 +258,8 @@ calib_sv_tc_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_consta
             pk[k >> 1] = pack_bf16x2(p0, p1);
           }
         }
-        // keys c0 .. c0 + 31 = 16-B chunks c0/8 .. c0/8 + 3 of key half c0 / 64
-        uint8_t* base = S.P[c0 >> 6] + r * 128;
+        // keys c0 .. c0 + 31 = 16-B chunks (c0 % 64)/8 .. + 3 of key half ch
+        uint8_t* base = S.P[ch] + r * 128;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int c16 = ((c0 & 63) >> 3) + q;
@@ -264,13 +275,16 @@ calib_sv_tc_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_consta
         mbar_arrive(&S.pfull);
       }
     }
-    // O / l -> SV bf16 [N][H_q][128]
+    // row sum of both halves, then O / l -> SV bf16 [N][H_q][128] (this warp's 64 channels)
+    S.xl[ch][r] = l;
+    asm volatile("bar.sync %0, 64;\n" ::"r"(1 + quarter) : "memory");
+    l += S.xl[ch ^ 1][r];
     mbar_wait(&S.pvfull, (nblk - 1) & 1);
     fence_after();
     const float inv = l > 0.f ? 1.f / l : 0.f;
     uint16_t* dst = p.SV + ((size_t)qi * p.hq + qh) * kD;
 #pragma unroll 1
-    for (int c0 = 0; c0 < kD; c0 += 32) {
+    for (int c0 = cb; c0 < cb + 64; c0 += 32) {
       uint32_t o[32];
       OSCAR_TMEM_LD32(trow + 256 + c0, o);
       tmem_ld_wait();
@@ -287,7 +301,7 @@ calib_sv_tc_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_consta
   }
   fence_before();
   __syncthreads();
-  if (warp == 5) {
+  if (warp == 9) {
     fence_after();
     tmem_dealloc(tmem, 512);
   }

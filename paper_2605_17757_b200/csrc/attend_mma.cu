@@ -580,7 +580,7 @@ attend_partial_mma(AttnParams p, int S) {
           // one ldmatrix.x4: matrices (rows 0-7 | 8-15) x (bytes 0-15 | 16-31) of the K tile, so
           // lane (gid, t) receives words t and 4 + t of rows gid and gid + 8
           uint32_t wa[NG == 4 ? 8 : 2], wb[NG == 4 ? 8 : 2];
-          uint32_t ha4[NG == 4 && BITS == 3 ? 4 : 1], hb4[NG == 4 && BITS == 3 ? 4 : 1];
+          [[maybe_unused]] uint32_t ha4[NG == 4 && BITS == 3 ? 4 : 1], hb4[NG == 4 && BITS == 3 ? 4 : 1];
           if constexpr (NG == 4) {
             // G = 32: lane t takes 2-bit field t of every word of rows gid / gid + 8 (k-step g =
             // words 2g, 2g + 1 = group g)
@@ -605,7 +605,7 @@ attend_partial_mma(AttnParams p, int S) {
           }
           // 3-bit: the high-plane words of low words t and 4 + t (high word j / 2, nibble j % 2
           // = t % 2) of rows gid / gid + 8, normalized so the lane's nibble sits in bits 4-7
-          uint32_t ha[2], hb[2];
+          [[maybe_unused]] uint32_t ha[2], hb[2];
           if constexpr (BITS == 3 && NG != 4) {
             const uint32_t* ra = reinterpret_cast<const uint32_t*>(pg + (size_t)(16 * st + gid) * RB + 32);
             const uint32_t* rb = reinterpret_cast<const uint32_t*>(pg + (size_t)(16 * st + 8 + gid) * RB + 32);
@@ -798,7 +798,7 @@ attend_partial_mma(AttnParams p, int S) {
           }
           // 3-bit: high-plane word k = high byte 4k + gid % 4 of this lane's 4 tokens (FORMAT,
           // reading Z36); the lane's nibble gid / 4 moved to bits 0-3 of each byte
-          uint32_t vh[BITS == 3 ? 4 : 1];
+          [[maybe_unused]] uint32_t vh[BITS == 3 ? 4 : 1];
           if constexpr (BITS == 3) {
             const uint4 x = *reinterpret_cast<const uint4*>(vcodes + (size_t)st * 16 * RB + 512 + 16 * (4 * (gid & 3) + t));
             const int sh = 4 * (gid >> 2);

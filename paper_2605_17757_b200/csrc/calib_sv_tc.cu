@@ -34,8 +34,7 @@ struct SvSmem {
   alignas(1024) uint8_t Q[2][kSvHalf];        // [channel half][query row][128 B]
   alignas(1024) uint8_t K[2][2][kSvHalf];     // [stage][channel half][key row][128 B]
   alignas(1024) uint8_t V[2][2][kSvHalf];     // [stage][channel half][key row][128 B]
-  alignas(1024) uint8_t P[2][kSvHalf];        // [key half][query row][128 B] (bf16 P, SW128)
-  uint64_t qfull, kvfull[2], kvempty[2], sfull[2], sempty[2], pfull, pvfull;
+  uint64_t qfull, kvfull[2], kvempty[2], sfull[2], sempty[2], pfull[2], pvdone[2];
   uint32_t tmem_base;
   float xmax[2][2][128];                      // [block parity][column half][row] softmax max exchange
   float xl[2][128];                           // [column half][row] final row sums
@@ -54,6 +53,27 @@ constexpr uint32_t kIdescPV = idesc_bf16(128, 128, false, true);   // B (V) MN-m
         "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]),            \
         "r"(v[29]), "r"(v[30]), "r"(v[31])                                                             \
       : "memory")
+
+// tcgen05.mma with A from tensor memory (M = 128 lanes, K packed two bf16 per 32-bit column, the
+// even k in the low half) and B from shared memory
+template <uint32_t IDESC>
+__device__ __forceinline__ void umma_f16_ts(uint32_t dt, uint32_t at, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n"
+      ::"r"(dt), "r"(at), "l"(b), "r"(IDESC), "r"(acc));
+}
+
+#define OSCAR_TMEM_ST16(base, v)                                                                     \
+  asm volatile(                                                                                       \
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"  \
+      "%15,%16};\n"                                                                                   \
+      ::"r"(base), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]),        \
+        "r"(v[7]), "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]),   \
+        "r"(v[15])                                                                                     \
+      : "memory")
+
+constexpr uint32_t kPCol = 384;               // TMEM columns of the two P buffers (64 each)
 
 // sequence containing token n: the last s with starts[s] <= n
 __device__ __forceinline__ int sv_seq_start(const int32_t* starts, int n_seq, int n) {
@@ -103,8 +123,7 @@ calib_sv_tc_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_consta
       mbar_init(&S.kvfull[s], 1); mbar_init(&S.kvempty[s], 1);
       mbar_init(&S.sfull[s], 1); mbar_init(&S.sempty[s], 8);
     }
-    mbar_init(&S.pfull, 8);
-    mbar_init(&S.pvfull, 1);
+    for (int s = 0; s < 2; ++s) { mbar_init(&S.pfull[s], 8); mbar_init(&S.pvdone[s], 1); }
     mbar_init_fence();
   }
   if (warp == 9) tmem_alloc(&S.tmem_base, 512);
@@ -149,15 +168,15 @@ calib_sv_tc_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_consta
       }
       if (j >= 1) {
         const int jj = j - 1, s = jj & 1;
-        mbar_wait(&S.pfull, jj & 1);
+        mbar_wait(&S.pfull[jj & 1], (jj >> 1) & 1);
         fence_after();
         if (lane == 0) {
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk)
-            umma_f16<kIdescPV>(tmem + 256, kmajor_sw128_desc(su32(S.P[kk >> 2]) + (kk & 3) * 32),
+            umma_f16_ts<kIdescPV>(tmem + 256, tmem + kPCol + 64 * (jj & 1) + 8 * kk,
                                mnmajor_sw128_desc(su32(S.V[s][0]) + kk * 2048, kSvHalf), (jj | kk) != 0);
           umma_commit(&S.kvempty[s]);     // K_jj, V_jj consumed
-          umma_commit(&S.pvfull);         // O holds blocks 0..jj; P free
+          umma_commit(&S.pvdone[jj & 1]); // O holds blocks 0..jj; P buffer jj % 2 free
         }
         __syncwarp();
       }
@@ -206,9 +225,9 @@ calib_sv_tc_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_consta
       S.xmax[b][ch][r] = bm;
       asm volatile("bar.sync %0, 64;\n" ::"r"(1 + quarter) : "memory");
       bm = fmaxf(bm, S.xmax[b][ch ^ 1][r]);
-      // P_{j-1}·V_{j-1} done: O may be rescaled and the P tile rewritten
-      if (j >= 1) {
-        mbar_wait(&S.pvfull, (j - 1) & 1);
+      // P buffer j % 2 free: P_{j-2}·V_{j-2} done
+      if (j >= 2) {
+        mbar_wait(&S.pvdone[j & 1], ((j >> 1) - 1) & 1);
         fence_after();
       }
       // (both warps of the row take the same decision; the TMEM load / store below are
@@ -220,6 +239,11 @@ calib_sv_tc_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_consta
       if (resc) { a = ex2(m - bm); l *= a; }
       if (upd) m = bm;
       if (__any_sync(0xffffffffu, resc)) {
+        // O holds blocks 0..j-1 once P_{j-1}·V_{j-1} is done (the MMAs complete in issue order)
+        if (j >= 1) {
+          mbar_wait(&S.pvdone[(j - 1) & 1], ((j - 1) >> 1) & 1);
+          fence_after();
+        }
 #pragma unroll 1
         for (int c0 = cb; c0 < cb + 64; c0 += 32) {
           uint32_t o[32];
@@ -258,28 +282,22 @@ calib_sv_tc_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_consta
             pk[k >> 1] = pack_bf16x2(p0, p1);
           }
         }
-        // keys c0 .. c0 + 31 = 16-B chunks (c0 % 64)/8 .. + 3 of key half ch
-        uint8_t* base = S.P[ch] + r * 128;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int c16 = ((c0 & 63) >> 3) + q;
-          *reinterpret_cast<uint4*>(base + ((c16 ^ (r & 7)) << 4)) =
-              make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-        }
+        // keys c0 .. c0 + 31 -> TMEM columns kPCol + 64·(j % 2) + c0 / 2 .. + 15 of this lane
+        OSCAR_TMEM_ST16(trow + kPCol + 64 * (j & 1) + c0 / 2, pk);
       }
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // P -> the MMA's async proxy
+      asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
       fence_before();
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(&S.sempty[b]);
-        mbar_arrive(&S.pfull);
+        mbar_arrive(&S.pfull[j & 1]);
       }
     }
     // row sum of both halves, then O / l -> SV bf16 [N][H_q][128] (this warp's 64 channels)
     S.xl[ch][r] = l;
     asm volatile("bar.sync %0, 64;\n" ::"r"(1 + quarter) : "memory");
     l += S.xl[ch ^ 1][r];
-    mbar_wait(&S.pvfull, (nblk - 1) & 1);
+    mbar_wait(&S.pvdone[(nblk - 1) & 1], ((nblk - 1) >> 1) & 1);
     fence_after();
     const float inv = l > 0.f ? 1.f / l : 0.f;
     uint16_t* dst = p.SV + ((size_t)qi * p.hq + qh) * kD;

@@ -6,16 +6,18 @@
 //
 // One CTA = 128 queries of one query head, 10 warps:
 //   warp 8  TMA producer: the Q tile once, then 128-key K and V tiles (two 64-channel SWIZZLE_128B
-//           boxes each) into a 2-stage ring
+//           boxes each) into a 3-stage K ring (a stage frees once its Q·Kᵀ completes) and a 2-stage
+//           V ring (freed by its P·V)
 //   warp 9  TMEM allocator + single-thread tcgen05.mma issuer:
 //             S_j  = Q·K_jᵀ      (A = Q K-major, B = K_j K-major)   -> TMEM columns 128·(j % 2)
-//             O   += P_j·V_j     (A = P_j K-major from smem, B = V_j MN-major) -> TMEM columns 256..383
+//             O   += P_j·V_j     (A = P_j from TMEM, B = V_j MN-major) -> TMEM columns 256..383
 //   warps 0-7  softmax (thread = query row = TMEM lane; warps q and q + 4 take key columns 0-63 /
 //           64-127 of the rows of lane quarter q, combining max and sum through smem): per key block, pass 1 reads S and forms
 //           the masked row max; the running max m moves only when the block max exceeds it by more
 //           than 2^8 (then O is rescaled in TMEM by exp2(m_old - m_new)), otherwise P ≤ 2^8 stays
-//           exact in range for bf16; pass 2 writes P = exp2(S·scale·log2e - m) as bf16 into the
-//           swizzled K-major smem tile the next P·V reads, and sums l.  At the end O / l -> SV bf16.
+//           exact in range for bf16; pass 2 writes P = exp2(S·scale·log2e - m) as bf16 into one
+//           of two TMEM P buffers (columns 384 / 448) the P·V MMA reads as its A operand, and sums
+//           l.  At the end O / l -> SV bf16.
 #include "common.cuh"
 #include "ptx.cuh"
 
@@ -28,13 +30,16 @@ constexpr int kSvQ = 128;                     // queries per CTA (UMMA M)
 constexpr int kSvK = 128;                     // keys per block
 constexpr int kSvHalf = 128 * 128;            // one 64-channel (or 64-key) half tile: 128 rows x 128 B
 constexpr int kSvThreads = 10 * 32;
+constexpr int kSvStages = 3;                  // K ring (a stage frees once its Q·Kᵀ completes)
+constexpr int kSvVStages = 2;                 // V ring (a stage frees once its P·V completes)
 constexpr float kRescaleThr = 8.f;            // log2 units
 
 struct SvSmem {
   alignas(1024) uint8_t Q[2][kSvHalf];        // [channel half][query row][128 B]
-  alignas(1024) uint8_t K[2][2][kSvHalf];     // [stage][channel half][key row][128 B]
-  alignas(1024) uint8_t V[2][2][kSvHalf];     // [stage][channel half][key row][128 B]
-  uint64_t qfull, kvfull[2], kvempty[2], sfull[2], sempty[2], pfull[2], pvdone[2];
+  alignas(1024) uint8_t K[kSvStages][2][kSvHalf];   // [stage][channel half][key row][128 B]
+  alignas(1024) uint8_t V[kSvVStages][2][kSvHalf];  // [stage][channel half][key row][128 B]
+  uint64_t qfull, kfull[kSvStages], kempty[kSvStages], vfull[kSvVStages], vempty[kSvVStages];
+  uint64_t sfull[2], sempty[2], pfull[2], pvdone[2];
   uint32_t tmem_base;
   float xmax[2][2][128];                      // [block parity][column half][row] softmax max exchange
   float xl[2][128];                           // [column half][row] final row sums
@@ -119,10 +124,9 @@ calib_sv_tc_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_consta
 
   if (threadIdx.x == 0) {
     mbar_init(&S.qfull, 1);
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&S.kvfull[s], 1); mbar_init(&S.kvempty[s], 1);
-      mbar_init(&S.sfull[s], 1); mbar_init(&S.sempty[s], 8);
-    }
+    for (int s = 0; s < kSvStages; ++s) { mbar_init(&S.kfull[s], 1); mbar_init(&S.kempty[s], 1); }
+    for (int s = 0; s < kSvVStages; ++s) { mbar_init(&S.vfull[s], 1); mbar_init(&S.vempty[s], 1); }
+    for (int s = 0; s < 2; ++s) { mbar_init(&S.sfull[s], 1); mbar_init(&S.sempty[s], 8); }
     for (int s = 0; s < 2; ++s) { mbar_init(&S.pfull[s], 8); mbar_init(&S.pvdone[s], 1); }
     mbar_init_fence();
   }
@@ -139,13 +143,16 @@ calib_sv_tc_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_consta
       tma_load_3d(S.Q[0], &mapQ, 0, qh, q0, &S.qfull);
       tma_load_3d(S.Q[1], &mapQ, 64, qh, q0, &S.qfull);
       for (int j = 0; j < nblk; ++j) {
-        const int s = j & 1, key0 = kbeg + j * kSvK;
-        mbar_wait(&S.kvempty[s], ((j >> 1) & 1) ^ 1);
-        mbar_expect_tx(&S.kvfull[s], 4 * kSvHalf);
-        tma_load_3d(S.K[s][0], &mapK, 0, h, key0, &S.kvfull[s]);
-        tma_load_3d(S.K[s][1], &mapK, 64, h, key0, &S.kvfull[s]);
-        tma_load_3d(S.V[s][0], &mapV, 0, h, key0, &S.kvfull[s]);
-        tma_load_3d(S.V[s][1], &mapV, 64, h, key0, &S.kvfull[s]);
+        const int s = j % kSvStages, ph = ((j / kSvStages) & 1) ^ 1, key0 = kbeg + j * kSvK;
+        mbar_wait(&S.kempty[s], ph);
+        mbar_expect_tx(&S.kfull[s], 2 * kSvHalf);
+        tma_load_3d(S.K[s][0], &mapK, 0, h, key0, &S.kfull[s]);
+        tma_load_3d(S.K[s][1], &mapK, 64, h, key0, &S.kfull[s]);
+        const int vs = j % kSvVStages;
+        mbar_wait(&S.vempty[vs], ((j / kSvVStages) & 1) ^ 1);
+        mbar_expect_tx(&S.vfull[vs], 2 * kSvHalf);
+        tma_load_3d(S.V[vs][0], &mapV, 0, h, key0, &S.vfull[vs]);
+        tma_load_3d(S.V[vs][1], &mapV, 64, h, key0, &S.vfull[vs]);
       }
     }
   } else if (warp == 9) {
@@ -153,21 +160,23 @@ calib_sv_tc_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_consta
     mbar_wait(&S.qfull, 0);
     for (int j = 0; j <= nblk; ++j) {
       if (j < nblk) {
-        const int s = j & 1;
-        mbar_wait(&S.kvfull[s], (j >> 1) & 1);
+        const int s = j & 1, ks = j % kSvStages;
+        mbar_wait(&S.kfull[ks], (j / kSvStages) & 1);
         mbar_wait(&S.sempty[s], ((j >> 1) & 1) ^ 1);
         fence_after();
         if (lane == 0) {
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk)
             umma_f16<kIdescS>(tmem + 128 * s, kmajor_sw128_desc(su32(S.Q[kk >> 2]) + (kk & 3) * 32),
-                              kmajor_sw128_desc(su32(S.K[s][kk >> 2]) + (kk & 3) * 32), kk != 0);
+                              kmajor_sw128_desc(su32(S.K[ks][kk >> 2]) + (kk & 3) * 32), kk != 0);
           umma_commit(&S.sfull[s]);
+          umma_commit(&S.kempty[ks]);     // K_j consumed
         }
         __syncwarp();
       }
       if (j >= 1) {
-        const int jj = j - 1, s = jj & 1;
+        const int jj = j - 1, s = jj % kSvVStages;
+        mbar_wait(&S.vfull[s], (jj / kSvVStages) & 1);
         mbar_wait(&S.pfull[jj & 1], (jj >> 1) & 1);
         fence_after();
         if (lane == 0) {
@@ -175,7 +184,7 @@ calib_sv_tc_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_consta
           for (int kk = 0; kk < 8; ++kk)
             umma_f16_ts<kIdescPV>(tmem + 256, tmem + kPCol + 64 * (jj & 1) + 8 * kk,
                                mnmajor_sw128_desc(su32(S.V[s][0]) + kk * 2048, kSvHalf), (jj | kk) != 0);
-          umma_commit(&S.kvempty[s]);     // K_jj, V_jj consumed
+          umma_commit(&S.vempty[s]);      // V_jj consumed
           umma_commit(&S.pvdone[jj & 1]); // O holds blocks 0..jj; P buffer jj % 2 free
         }
         __syncwarp();

@@ -984,7 +984,10 @@ cudaError_t launch_attend(const oscar_ctx& c, const void* q, const int32_t* page
   }
   {
     // small batches: one CTA per query head (the fold of many splits gets 8 warps per head)
-    const bool per_head = (long)B * c.hkv * 4 <= (long)c.num_sms;
+#ifndef OSCAR_MERGE_PER_HEAD_MUL
+#define OSCAR_MERGE_PER_HEAD_MUL 4
+#endif
+    const bool per_head = (long)B * c.hkv * OSCAR_MERGE_PER_HEAD_MUL <= (long)c.num_sms;
     void (*fn)(AttnParams, const float*, void*, int, float*, StepParams) =
         per_head ? attend_merge_kernel<1>
       : c.g == 1 ? attend_merge_kernel<1> : c.g == 2 ? attend_merge_kernel<2>

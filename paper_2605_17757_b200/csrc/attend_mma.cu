@@ -1001,8 +1001,11 @@ KernelFn pick(int bits, int g, int ng) {
 
 // ring stages per warp: 2-4 within ~48 KB per CTA; large pages (P = 256 at 4 bits: 36 KB) fall
 // back to what fits in the 227-KB CTA limit (1 stage), 0 if not even that
+#ifndef OSCAR_RING_KB
+#define OSCAR_RING_KB 48
+#endif
 int stages_for(int page_bytes) {
-  int S = (48 * 1024) / (kWarps * page_bytes);
+  int S = (OSCAR_RING_KB * 1024) / (kWarps * page_bytes);
   S = S < 2 ? 2 : (S > 4 ? 4 : S);
   while (S > 0 && kWarps * S * (page_bytes + 8) > 227 * 1024) --S;
   return S;

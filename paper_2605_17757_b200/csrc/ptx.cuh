@@ -1,7 +1,7 @@
 // L0 device primitives for sm_100a: mbarrier, TMA / cp.async.bulk, tcgen05
 // (UMMA descriptors, mma issue, commit, TMEM loads) and the host-side tensor-map encoder.
 // Header-only; shared by every kernel file that uses them (append_tc.cu, calib_tc.cu,
-// attend_mma.cu).  Not part of the ABI.
+// calib_sv_tc.cu, attend.cu, attend_mma.cu).  Not part of the ABI.
 #pragma once
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -118,6 +118,36 @@ __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.
         "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),       \
         "=r"(v[14]), "=r"(v[15])                                                                       \
       : "r"(base))
+
+#define OSCAR_TMEM_ST32(base, v)                                                                     \
+  asm volatile(                                                                                       \
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"  \
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};\n"                   \
+      ::"r"(base), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]),        \
+        "r"(v[7]), "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]),   \
+        "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]),            \
+        "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]),            \
+        "r"(v[29]), "r"(v[30]), "r"(v[31])                                                             \
+      : "memory")
+
+// tcgen05.mma with A from tensor memory (M = 128 lanes, K packed two bf16 per 32-bit column, the
+// even k in the low half) and B from shared memory
+template <uint32_t IDESC>
+__device__ __forceinline__ void umma_f16_ts(uint32_t dt, uint32_t at, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n"
+      ::"r"(dt), "r"(at), "l"(b), "r"(IDESC), "r"(acc));
+}
+
+#define OSCAR_TMEM_ST16(base, v)                                                                     \
+  asm volatile(                                                                                       \
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"  \
+      "%15,%16};\n"                                                                                   \
+      ::"r"(base), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]),        \
+        "r"(v[7]), "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]),   \
+        "r"(v[15])                                                                                     \
+      : "memory")
 
 // ---------------------------------------------------------------- host: tensor-map encoder
 // cuTensorMapEncodeTiled through the runtime's driver entry point; resolved once (a function-

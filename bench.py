@@ -473,6 +473,8 @@ def main():
     if args.c5_only:
         if rank == 0:
             emit(c5_leg(args, dev, hbm_peak))
+        if dist.is_initialized():
+            dist.destroy_process_group()
         return
     if args.c4_only:
         gen = torch.Generator(device=dev).manual_seed(1234 + rank)
@@ -481,6 +483,8 @@ def main():
         r = c4_leg(args, world, rank, dev, gen, RK, RV, hbm_peak, peak_kind)
         if rank == 0:
             emit(r)
+        if dist.is_initialized():
+            dist.destroy_process_group()
         return
     o = Bnd.Oscar(Bnd.Config(num_q_heads=HQ, num_kv_heads=HKV, bits=BITS, group_size=G, page_size=P))
     o.set_variant(args.variant)

@@ -13,7 +13,8 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2605_17757_b200 import binding as Bnd, synth  # noqa: E402
 
-HQ, HKV, D, P, NL, B, L = 32, 8, 128, 64, 8, 16, 32768
+HQ, HKV, D, P, NL, L = 32, 8, 128, 64, 8, 32768
+B = int(os.environ.get("OSCAR_TL_B", "16"))
 FN = os.environ.get("OSCAR_TL_FN", "decode_step")
 dev = "cuda"
 gen = torch.Generator(device=dev).manual_seed(3)

@@ -103,7 +103,9 @@ OSCAR_API oscar_status oscar_calib_accumulate(const oscar_ctx* ctx, const void* 
 /* S·V on the device for the C_S target: SV = softmax(Q Kᵀ·scale + M) V per query
  * head (Alg. 1), M causal including the diagonal and block-diagonal
  * across the calibration sequences (reading Z16); query head i attends KV head i/g.  Computed by a
- * flash-attention forward on the tensor cores (mma.sync bf16, fp32 softmax / accumulation).
+ * flash-attention forward on the tensor cores: variant 0 on tcgen05 (TMA tiles, S and O in TMEM;
+ * needs 16-B aligned Q, K, V, otherwise the variant-1 kernel runs), variant 1 on mma.sync; both
+ * bf16 operands with P rounded to bf16, fp32 softmax statistics and accumulation.
  * Q: bf16 [N][H_q][d]; K, V: bf16 [N][H_kv][d]; seq_starts: device int32 [n_seq], the first
  * token of each calibration sequence (seq_starts[0] = 0, strictly increasing, < N); SV: bf16
  * [N][H_q][d] (output; pass it to oscar_calib_accumulate as SV).  N = 0 is a no-op. */

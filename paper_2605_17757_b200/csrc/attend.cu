@@ -17,10 +17,14 @@
 #define OSCAR_PDL_MERGE 1
 #endif
 
+#ifndef OSCAR_CARVEOUT
+#define OSCAR_CARVEOUT 1
+#endif
+
 namespace oscar {
 
 // ------------------------------------------------------------------ prologue
-// q rotation (B1): grid (B, H_kv), 512 threads (16 warps).  Rows rotated per CTA: the GQ query
+// q rotation (B1): grid (B, H_kv), 256 threads (8 warps; 16 for g = 8).  Rows rotated per CTA: the GQ query
 // heads of group h by R_K[h].  Warp w owns the contraction slice k = 8w .. 8w+7: it loads those
 // 8 rows of R_K once — lane l the float4 of columns 4l..4l+3, 8 loads in flight — and forms
 // partial dots for every query row; the 16 partials per (row, channel) are summed through smem.
@@ -72,9 +76,16 @@ struct PrologueParams {
   unsigned long long* tl;       // timing probe (OSCAR_PROBE_TL)
 };
 
+// warps of the prologue: 8 (16 for g = 8: g q-row warps + the K and V row warps), so that two
+// partial-kernel CTAs fit beside it on an SM (64 registers per thread, 16 K per CTA)
 template <int GQ>
-__global__ void __launch_bounds__(512) attend_prologue_kernel(PrologueParams pp) {
+constexpr int kProWarps = GQ + 2 <= 8 ? 8 : 16;
+
+template <int GQ>
+__global__ void __launch_bounds__(kProWarps<GQ> * 32, 512 / (kProWarps<GQ> * 32) * 2)
+attend_prologue_kernel(PrologueParams pp) {
   constexpr int NR = GQ + 2;                         // q heads, then the decode step's K and V rows
+  constexpr int NW = kProWarps<GQ>, NT = NW * 32, KW = kD / NW;   // warps, threads, R rows per warp
   // dynamic smem: R_K[h] (64 KB) then R_V[h] (64 KB, decode step), bulk-copied before the wait;
   // the [16][NR][128] partial dots reuse it once every warp has finished its dots
   extern __shared__ __align__(128) float psm[];
@@ -116,7 +127,7 @@ __global__ void __launch_bounds__(512) attend_prologue_kernel(PrologueParams pp)
   if (pp.work && b == 0 && h == 0 && tid == 0) *pp.work = 0;   // reset the work-item counter
   // balanced decomposition: split count of sequence b (warp 15, CTA h = 0; loads overlapping the
   // rotation), the same formula as the partial kernel's Decomp::rof
-  if (pp.balanced && h == 0 && w == 15) {
+  if (pp.balanced && h == 0 && w == NW - 1) {
     int lt = 0, tot = 0;
     for (int bb = lane; bb < pp.batch; bb += 32) {
       const int n = (max(pp.seq_lens[bb] - pp.len_adj, 0) + pp.P - 1) / pp.P;
@@ -145,7 +156,7 @@ __global__ void __launch_bounds__(512) attend_prologue_kernel(PrologueParams pp)
   return;                                            // timing probe only (results invalid)
 #endif
   const int nrow = step ? NR : GQ;
-  for (int e = tid; e < nrow * (kD / 4); e += 512) {
+  for (int e = tid; e < nrow * (kD / 4); e += NT) {
     const int r = e >> 5, l4 = e & 31;
     const uint16_t* src = r < GQ ? pp.q + ((size_t)b * pp.Hq + (size_t)h * GQ + r) * kD
                                  : (r == GQ ? pp.knew : pp.vnew) + ((size_t)b * gridDim.y + h) * kD;
@@ -160,23 +171,23 @@ __global__ void __launch_bounds__(512) attend_prologue_kernel(PrologueParams pp)
     slot = (int64_t)pp.page_table[(size_t)b * pp.max_pages + pos / pp.ep.P] * pp.ep.P + pos % pp.ep.P;
   }
   ptx::mbar_wait(&rbar, 0);                          // R_K (R_V) resident
-  // warp w contracts rows 8w..8w+7 of R (lane: columns 4l..4l+3)
+  // warp w contracts rows KW·w .. KW·w + KW - 1 of R (lane: columns 4l..4l+3)
   float4 acc[NR];
 #pragma unroll
   for (int r = 0; r < NR; ++r) acc[r] = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const float4 mk = reinterpret_cast<const float4*>(Rks + (size_t)(8 * w + i) * kD)[lane];
+  for (int i = 0; i < KW; ++i) {
+    const float4 mk = reinterpret_cast<const float4*>(Rks + (size_t)(KW * w + i) * kD)[lane];
 #pragma unroll
     for (int r = 0; r < GQ + 1; ++r) {
       if (r == GQ && !step) break;
-      const float x = xs[r][8 * w + i];
+      const float x = xs[r][KW * w + i];
       acc[r].x = fmaf(x, mk.x, acc[r].x); acc[r].y = fmaf(x, mk.y, acc[r].y);
       acc[r].z = fmaf(x, mk.z, acc[r].z); acc[r].w = fmaf(x, mk.w, acc[r].w);
     }
     if (rotv) {
-      const float4 mv = reinterpret_cast<const float4*>(Rvs + (size_t)(8 * w + i) * kD)[lane];
-      const float x = xs[GQ + 1][8 * w + i];
+      const float4 mv = reinterpret_cast<const float4*>(Rvs + (size_t)(KW * w + i) * kD)[lane];
+      const float x = xs[GQ + 1][KW * w + i];
       acc[GQ + 1].x = fmaf(x, mv.x, acc[GQ + 1].x); acc[GQ + 1].y = fmaf(x, mv.y, acc[GQ + 1].y);
       acc[GQ + 1].z = fmaf(x, mv.z, acc[GQ + 1].z); acc[GQ + 1].w = fmaf(x, mv.w, acc[GQ + 1].w);
     }
@@ -189,14 +200,14 @@ __global__ void __launch_bounds__(512) attend_prologue_kernel(PrologueParams pp)
     reinterpret_cast<float4*>(ps + ((size_t)w * NR + r) * kD)[lane] = acc[r];
   }
   __syncthreads();
-  for (int e = tid; e < nrow * kD; e += 512) {
+  for (int e = tid; e < nrow * kD; e += NT) {
     const int r = e >> 7, c = e & (kD - 1);
     float y = 0.f;
     if (r == GQ + 1 && !rotv) {
       y = xs[r][c];                                  // pre-rotated V (NEXT-2): identity
     } else {
 #pragma unroll
-      for (int ww = 0; ww < 16; ++ww) y += ps[((size_t)ww * NR + r) * kD + c];
+      for (int ww = 0; ww < NW; ++ww) y += ps[((size_t)ww * NR + r) * kD + c];
     }
     ys[r][c] = y;
   }
@@ -250,10 +261,10 @@ __global__ void __launch_bounds__(512) attend_prologue_kernel(PrologueParams pp)
     for (int o = 1; o < (G >> 2); o <<= 1) gs += __shfl_xor_sync(0xffffffffu, gs, o);
     if ((lane & ((G >> 2) - 1)) == 0) pp.qsum[row * 8 + (lane * 4 >> pp.lgG)] = gs;
   }
-  if (step) asm volatile("bar.sync 1, %0;\n" ::"r"(512 - 64) : "memory");   // all but warps GQ, GQ + 1
+  if (step) asm volatile("bar.sync 1, %0;\n" ::"r"(NT - 64) : "memory");   // all but warps GQ, GQ + 1
   else __syncthreads();
   // the fragment writers: every thread still running, renumbered 0 .. nft - 1
-  const int ft = step && w > GQ + 1 ? tid - 64 : tid, nft = step ? 512 - 64 : 512;
+  const int ft = step && w > GQ + 1 ? tid - 64 : tid, nft = step ? NT - 64 : NT;
   // IMMA A fragments for attend_partial_mma: word (j, kk, r) of lane (gid, t) holds the
   // hi (r even) / lo (r odd) int8 of qint[head][channel] for combo 8j + gid = grp·g + head,
   // zero outside the combo's group (see attend_mma.cu)
@@ -938,15 +949,22 @@ cudaError_t launch_attend(const oscar_ctx& c, const void* q, const int32_t* page
     pp.tl = g_tl;
     void (*fn)(PrologueParams) = c.g == 1 ? attend_prologue_kernel<1> : c.g == 2 ? attend_prologue_kernel<2>
                                : c.g == 4 ? attend_prologue_kernel<4> : attend_prologue_kernel<8>;
-    const int psmem = std::max(16 * (c.g + 2) * kD, (k_new && RV ? 2 : 1) * kD * kD) * (int)sizeof(float);
+    const int pnw = c.g + 2 <= 8 ? 8 : 16;
+    const int psmem = std::max(pnw * (c.g + 2) * kD, (k_new && RV ? 2 : 1) * kD * kD) * (int)sizeof(float);
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, psmem);
     if (e != cudaSuccess) return e;
+#if OSCAR_CARVEOUT
+    // full shared-memory carveout on the prologue and the partial kernel, so that partial CTAs
+    // can become resident beside the prologue's
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e != cudaSuccess) return e;
+#endif
     // PDL launch: its CTAs may become resident while the previous kernel of the stream drains;
     // the kernel's first instruction waits for that kernel's completion, so every later read
     // (and the partial kernel's early page prefetch) sees the caller's writes
     cudaLaunchConfig_t pcfg{};
     pcfg.gridDim = dim3((unsigned)B, (unsigned)c.hkv);
-    pcfg.blockDim = dim3(512);
+    pcfg.blockDim = dim3(32 * pnw);
     pcfg.dynamicSmemBytes = psmem;
     pcfg.stream = s;
     pcfg.attrs = pdl;

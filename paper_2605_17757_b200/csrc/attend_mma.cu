@@ -29,6 +29,10 @@
 #include "attend_common.cuh"
 #include "ptx.cuh"
 
+#ifndef OSCAR_CARVEOUT
+#define OSCAR_CARVEOUT 1
+#endif
+
 namespace oscar {
 
 namespace {
@@ -1057,6 +1061,10 @@ cudaError_t launch_attend_mma(const AttnParams& p, cudaStream_t s) {
   const int smem = mma_smem(p.page_bytes, p.batch);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
+#if OSCAR_CARVEOUT
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);   // see launch_attend
+  if (e != cudaSuccess) return e;
+#endif
   const int grid = p.n_warps / kWarps;
   // programmatic dependent launch: the first page loads overlap attend_prologue_kernel;
   // griddepcontrol.wait in the kernel orders every read of the prologue's outputs

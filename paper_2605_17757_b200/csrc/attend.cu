@@ -24,10 +24,10 @@
 namespace oscar {
 
 // ------------------------------------------------------------------ prologue
-// q rotation (B1): grid (B, H_kv), 256 threads (8 warps; 16 for g = 8).  Rows rotated per CTA: the GQ query
-// heads of group h by R_K[h].  Warp w owns the contraction slice k = 8w .. 8w+7: it loads those
-// 8 rows of R_K once — lane l the float4 of columns 4l..4l+3, 8 loads in flight — and forms
-// partial dots for every query row; the 16 partials per (row, channel) are summed through smem.
+// q rotation (B1): grid (B, H_kv), NW = 8 warps (16 for g = 8).  Rows rotated per CTA: the GQ
+// query heads of group h by R_K[h] (staged in smem, see below).  Warp w owns the contraction slice
+// of 128 / NW rows of R_K (lane l: columns 4l..4l+3) and forms partial dots for every row; the NW
+// partials per (row, channel) are summed through smem.
 // Then:
 //   * warps 0..GQ-1: q̃ = q·R_K·scale·log₂e (fp32, kept for the simple kernel and for the decode
 //     step's new-token logit) and the 15-bit integer form of the IMMA QK path: qscale = max|q̃| /

@@ -451,6 +451,9 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
+        # NCCL's INFO log (nranks, transports, NVLS) goes to stderr with the rest of the library
+        # output (claim_stdout), so a scaling run can be checked against it
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
         dist.init_process_group("nccl", device_id=dev)
     elif not args.no_extras:
         # a 1-rank NCCL group, so the calibration all-reduce (the path's one collective) runs NCCL
@@ -887,6 +890,8 @@ def main():
                             "GBps": step_bytes * world * args.steps / (ms_stream * 1e-3) / 1e9},
         "clocks": clk.summary(),
         "variant": args.variant,
+        "process_group": ({"backend": dist.get_backend(), "world_size": dist.get_world_size()}
+                          if dist.is_initialized() else None),
     }
     if e2e:
         line["e2e"] = e2e

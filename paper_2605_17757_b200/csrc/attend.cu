@@ -550,7 +550,10 @@ struct StepParams {
 };
 
 template <int HC>
-__global__ void __launch_bounds__(256) attend_merge_kernel(AttnParams p, const float* __restrict__ RV,
+#ifndef OSCAR_MERGE_MINB
+#define OSCAR_MERGE_MINB 1
+#endif
+__global__ void __launch_bounds__(256, OSCAR_MERGE_MINB) attend_merge_kernel(AttnParams p, const float* __restrict__ RV,
                                                            void* __restrict__ out, int out_fp32,
                                                            float* __restrict__ lse, StepParams sp) {
 #ifdef OSCAR_PROBE_NOMERGE
@@ -1017,6 +1020,10 @@ cudaError_t launch_attend(const oscar_ctx& c, const void* q, const int32_t* page
     sp.seq_lens = seq_lens;
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, msmem);
     if (e != cudaSuccess) return e;
+#if OSCAR_CARVEOUT
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e != cudaSuccess) return e;
+#endif
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)B, (unsigned)c.hkv, (unsigned)(c.g / hc));
     cfg.blockDim = dim3(256);

@@ -288,6 +288,14 @@ attend_partial_mma(AttnParams p, int S) {
   // the first pages depend only on the caller's inputs: start streaming before the prologue ends
   while (inflight < S && issue_one()) {}
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
+#ifndef OSCAR_PARTIAL_EARLY_TRIGGER
+#define OSCAR_PARTIAL_EARLY_TRIGGER 1
+#endif
+#if OSCAR_PARTIAL_EARLY_TRIGGER
+  // the merge grid may launch now (the prologue is complete): its CTAs take the SMs' resources as
+  // partial CTAs retire and do their pre-wait work beside this grid's tail
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+#endif
   if (lane == 0) tl_mark(p.tl, 1, gw, 1);
   while (inflight < S && issue_one()) {}
 

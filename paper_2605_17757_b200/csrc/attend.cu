@@ -80,9 +80,16 @@ struct PrologueParams {
 // partial-kernel CTAs fit beside it on an SM (64 registers per thread, 16 K per CTA)
 template <int GQ>
 constexpr int kProWarps = GQ + 2 <= 8 ? 8 : 16;
+// 8 warps: <= 64 registers (two partial CTAs beside the prologue CTA); 16 warps (g = 8): one
+// partial CTA fits either way, so the register cap is left at 128 (no spills)
+#ifndef OSCAR_PRO16_MINB
+#define OSCAR_PRO16_MINB 1
+#endif
+template <int GQ>
+constexpr int kProMinBlocks = kProWarps<GQ> == 8 ? 4 : OSCAR_PRO16_MINB;
 
 template <int GQ>
-__global__ void __launch_bounds__(kProWarps<GQ> * 32, 512 / (kProWarps<GQ> * 32) * 2)
+__global__ void __launch_bounds__(kProWarps<GQ> * 32, kProMinBlocks<GQ>)
 attend_prologue_kernel(PrologueParams pp) {
   constexpr int NR = GQ + 2;                         // q heads, then the decode step's K and V rows
   constexpr int NW = kProWarps<GQ>, NT = NW * 32, KW = kD / NW;   // warps, threads, R rows per warp

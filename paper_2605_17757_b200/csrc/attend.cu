@@ -534,10 +534,13 @@ __global__ void __launch_bounds__(128) attend_partial_simple(AttnParams p) {
 // LSE merge of the split-K partials + un-rotation o = õ·R_Vᵀ (reading Z21).
 // grid (B, H_kv, g / HC), 256 threads (8 warps): one CTA per (sequence, KV head) and HC query
 // heads of its group — HC = g normally (the heads share one copy of R_V[h]), HC = 1 for small
-// batches (more CTAs, more warps per head's splits).  Before griddepcontrol.wait (it only touches the
-// caller's inputs and the prologue's q̃) R_V[h] (64 KB) is bulk-copied into smem.  Then warp w serves head w mod g,
-// splits s ≡ w / g (mod 8/g): each lane issues all loads of a batch of up to 16 splits at once
-// (partial row float4 = channels 4l..4l+3, split max and sum) and folds them with a running max;
+// batches (more CTAs, more warps per head's splits).  Launched with PDL: the tensor-core partial
+// kernel triggers it right after its own wait (the prologue is complete), so its CTAs become
+// resident as partial CTAs retire; before griddepcontrol.wait it touches only the caller's inputs
+// and the prologue's outputs: R_V[h] (64 KB) bulk-copied into smem, the split count, the decode
+// step's new-token logit and v̂.  Then warp w serves head w mod g, splits s ≡ w / g (mod 8/g):
+// each lane loads batches of 4 splits, two batches in flight (partial row float4 = channels
+// 4l..4l+3, split max and sum) and folds them with a running max;
 // the 8/g warps of a head and the NEXT-1 segment are combined through smem.  Un-rotation:
 // thread (c', half) forms output channel c' of every other head from smem, the contraction index
 // rotated by lane % 8 (c = 4·((k + lane mod 8) mod 32)): conflict-free R_V rows, broadcast õ.

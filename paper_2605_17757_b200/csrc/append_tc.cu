@@ -45,7 +45,10 @@ constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr int kTileBytes = kTok * kD * 2;       // 32 KB bf16 tile
 constexpr int kBBytes = kD * kD * 2;            // 32 KB bf16 R part
 
-constexpr int kVStage = 2 * (16 * 64 + 16);    // V codes of one 32-token quarter (b <= 4), 2 padded tiles
+#ifndef OSCAR_VSTAGE_PAD
+#define OSCAR_VSTAGE_PAD 64      // 64 B: the two staged tiles of a half-warp pair land on disjoint banks (4-bit 0.629 -> 0.625 ms)
+#endif
+constexpr int kVStage = 2 * (16 * 64 + OSCAR_VSTAGE_PAD);   // V codes of one 32-token quarter (b <= 4), 2 padded tiles
 
 struct TcSmem {
   alignas(1024) uint8_t Bhi[kBBytes];           // [2 k-chunks][128 rows n][128 B], SW128
@@ -507,7 +510,7 @@ append_tc_kernel(const __grid_constant__ CUtensorMap mapK, const __grid_constant
                 make_uint4(packed[4 * w4], packed[4 * w4 + 1], packed[4 * w4 + 2], packed[4 * w4 + 3]);
         }
       } else if (fastV) {
-        constexpr int TILE = 16 * RB + 16;        // staged 16-token tile (+16 B: bank shift)
+        constexpr int TILE = 16 * RB + OSCAR_VSTAGE_PAD;   // staged 16-token tile (+ pad: bank shift)
         const uint32_t stg = su32(S.vstage[par][quarter]);
         // this token's bytes at their FORMAT offsets inside its 16-token tile (fmt_vbyte is
         // additive: the token part fmt_vbyte(u, 0) + the compile-time byte part fmt_vbyte(0, j))

@@ -4,7 +4,9 @@
 // sequences; query head i uses KV head i/g.  Same result as calib_sv.cu (the mma.sync kernel,
 // variant 1) up to fp32 summation order: P is rounded to bf16 before the P·V product in both.
 //
-// One CTA = 128 queries of one query head, 10 warps:
+// Persistent: one CTA per SM walks the (128-query block, query head) items, longest key ranges
+// first, its rings' phases running on across items (Q and O are handed over through qempty /
+// oempty).  One item = 128 queries of one query head; 10 warps:
 //   warp 8  TMA producer: the Q tile once, then 128-key K and V tiles (two 64-channel SWIZZLE_128B
 //           boxes each) into a 3-stage K ring (a stage frees once its Q·Kᵀ completes) and a 2-stage
 //           V ring (freed by its P·V)
@@ -39,7 +41,7 @@ struct SvSmem {
   alignas(1024) uint8_t K[kSvStages][2][kSvHalf];   // [stage][channel half][key row][128 B]
   alignas(1024) uint8_t V[kSvVStages][2][kSvHalf];  // [stage][channel half][key row][128 B]
   uint64_t qfull, kfull[kSvStages], kempty[kSvStages], vfull[kSvVStages], vempty[kSvVStages];
-  uint64_t sfull[2], sempty[2], pfull[2], pvdone[2];
+  uint64_t sfull[2], sempty[2], pfull[2], pvdone[2], qempty, oempty;
   uint32_t tmem_base;
   float xmax[2][2][128];                      // [block parity][column half][row] softmax max exchange
   float xl[2][128];                           // [column half][row] final row sums
@@ -85,15 +87,23 @@ calib_sv_tc_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_consta
   extern __shared__ uint8_t smem_raw[];
   SvSmem& S = *reinterpret_cast<SvSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int qb = p.nqb - 1 - (int)blockIdx.x;          // longest key ranges first
-  const int qh = blockIdx.y, h = qh / (p.hq / p.hkv);
-  const int q0 = qb * kSvQ;
-  const int qlast = min(q0 + kSvQ, p.N) - 1;
-  const int kbeg = sv_seq_start(p.starts, p.n_seq, q0);
-  const int nblk = (qlast - kbeg) / kSvK + 1;
+  // persistent: this CTA takes items it = blockIdx.x, blockIdx.x + gridDim.x, ... of the
+  // (query block, query head) list, longest key ranges first; the rings' phases run on across
+  // items (J = blocks this CTA has processed)
+  const int n_items = p.nqb * p.hq;
+  auto item = [&](int it, int& q0, int& qh, int& kbeg, int& nblk) {
+    const int qb = p.nqb - 1 - it / p.hq;
+    qh = it % p.hq;
+    q0 = qb * kSvQ;
+    const int qlast = min(q0 + kSvQ, p.N) - 1;
+    kbeg = sv_seq_start(p.starts, p.n_seq, q0);
+    nblk = (qlast - kbeg) / kSvK + 1;
+  };
 
   if (threadIdx.x == 0) {
     mbar_init(&S.qfull, 1);
+    mbar_init(&S.qempty, 1);
+    mbar_init(&S.oempty, 8);
     for (int s = 0; s < kSvStages; ++s) { mbar_init(&S.kfull[s], 1); mbar_init(&S.kempty[s], 1); }
     for (int s = 0; s < kSvVStages; ++s) { mbar_init(&S.vfull[s], 1); mbar_init(&S.vempty[s], 1); }
     for (int s = 0; s < 2; ++s) { mbar_init(&S.sfull[s], 1); mbar_init(&S.sempty[s], 8); }
@@ -109,56 +119,72 @@ calib_sv_tc_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_consta
   if (warp == 8) {
     // ================= TMA producer
     if (lane == 0) {
-      mbar_expect_tx(&S.qfull, 2 * kSvHalf);
-      tma_load_3d(S.Q[0], &mapQ, 0, qh, q0, &S.qfull);
-      tma_load_3d(S.Q[1], &mapQ, 64, qh, q0, &S.qfull);
-      for (int j = 0; j < nblk; ++j) {
-        const int s = j % kSvStages, ph = ((j / kSvStages) & 1) ^ 1, key0 = kbeg + j * kSvK;
-        mbar_wait(&S.kempty[s], ph);
-        mbar_expect_tx(&S.kfull[s], 2 * kSvHalf);
-        tma_load_3d(S.K[s][0], &mapK, 0, h, key0, &S.kfull[s]);
-        tma_load_3d(S.K[s][1], &mapK, 64, h, key0, &S.kfull[s]);
-        const int vs = j % kSvVStages;
-        mbar_wait(&S.vempty[vs], ((j / kSvVStages) & 1) ^ 1);
-        mbar_expect_tx(&S.vfull[vs], 2 * kSvHalf);
-        tma_load_3d(S.V[vs][0], &mapV, 0, h, key0, &S.vfull[vs]);
-        tma_load_3d(S.V[vs][1], &mapV, 64, h, key0, &S.vfull[vs]);
+      int J = 0, n = 0;
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++n) {
+        int q0, qh, kbeg, nblk;
+        item(it, q0, qh, kbeg, nblk);
+        const int h = qh / (p.hq / p.hkv);
+        if (n >= 1) mbar_wait(&S.qempty, (n - 1) & 1);   // the previous item's Q·Kᵀ are done
+        mbar_expect_tx(&S.qfull, 2 * kSvHalf);
+        tma_load_3d(S.Q[0], &mapQ, 0, qh, q0, &S.qfull);
+        tma_load_3d(S.Q[1], &mapQ, 64, qh, q0, &S.qfull);
+        for (int j = 0; j < nblk; ++j, ++J) {
+          const int s = J % kSvStages, ph = ((J / kSvStages) & 1) ^ 1, key0 = kbeg + j * kSvK;
+          mbar_wait(&S.kempty[s], ph);
+          mbar_expect_tx(&S.kfull[s], 2 * kSvHalf);
+          tma_load_3d(S.K[s][0], &mapK, 0, h, key0, &S.kfull[s]);
+          tma_load_3d(S.K[s][1], &mapK, 64, h, key0, &S.kfull[s]);
+          const int vs = J % kSvVStages;
+          mbar_wait(&S.vempty[vs], ((J / kSvVStages) & 1) ^ 1);
+          mbar_expect_tx(&S.vfull[vs], 2 * kSvHalf);
+          tma_load_3d(S.V[vs][0], &mapV, 0, h, key0, &S.vfull[vs]);
+          tma_load_3d(S.V[vs][1], &mapV, 64, h, key0, &S.vfull[vs]);
+        }
       }
     }
   } else if (warp == 9) {
     // ================= MMA issuer: S_j, then P_{j-1}·V_{j-1}
-    mbar_wait(&S.qfull, 0);
-    for (int j = 0; j <= nblk; ++j) {
-      if (j < nblk) {
-        const int s = j & 1, ks = j % kSvStages;
-        mbar_wait(&S.kfull[ks], (j / kSvStages) & 1);
-        mbar_wait(&S.sempty[s], ((j >> 1) & 1) ^ 1);
-        fence_after();
-        if (lane == 0) {
+    int J0 = 0, n = 0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++n) {
+      int q0, qh, kbeg, nblk;
+      item(it, q0, qh, kbeg, nblk);
+      mbar_wait(&S.qfull, n & 1);
+      for (int j = 0; j <= nblk; ++j) {
+        if (j < nblk) {
+          const int J = J0 + j, s = J & 1, ks = J % kSvStages;
+          mbar_wait(&S.kfull[ks], (J / kSvStages) & 1);
+          mbar_wait(&S.sempty[s], ((J >> 1) & 1) ^ 1);
+          fence_after();
+          if (lane == 0) {
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk)
-            umma_f16<kIdescS>(tmem + 128 * s, kmajor_sw128_desc(su32(S.Q[kk >> 2]) + (kk & 3) * 32),
-                              kmajor_sw128_desc(su32(S.K[ks][kk >> 2]) + (kk & 3) * 32), kk != 0);
-          umma_commit(&S.sfull[s]);
-          umma_commit(&S.kempty[ks]);     // K_j consumed
+            for (int kk = 0; kk < 8; ++kk)
+              umma_f16<kIdescS>(tmem + 128 * s, kmajor_sw128_desc(su32(S.Q[kk >> 2]) + (kk & 3) * 32),
+                                kmajor_sw128_desc(su32(S.K[ks][kk >> 2]) + (kk & 3) * 32), kk != 0);
+            umma_commit(&S.sfull[s]);
+            umma_commit(&S.kempty[ks]);     // K_j consumed
+            if (j == nblk - 1) umma_commit(&S.qempty);   // Q free for the next item
+          }
+          __syncwarp();
         }
-        __syncwarp();
-      }
-      if (j >= 1) {
-        const int jj = j - 1, s = jj % kSvVStages;
-        mbar_wait(&S.vfull[s], (jj / kSvVStages) & 1);
-        mbar_wait(&S.pfull[jj & 1], (jj >> 1) & 1);
-        fence_after();
-        if (lane == 0) {
+        if (j >= 1) {
+          const int jj = j - 1, JJ = J0 + jj, s = JJ % kSvVStages;
+          mbar_wait(&S.vfull[s], (JJ / kSvVStages) & 1);
+          mbar_wait(&S.pfull[JJ & 1], (JJ >> 1) & 1);
+          // the first P·V of an item overwrites O: the previous item's O must have been read
+          if (jj == 0 && n >= 1) mbar_wait(&S.oempty, (n - 1) & 1);
+          fence_after();
+          if (lane == 0) {
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk)
-            umma_f16_ts<kIdescPV>(tmem + 256, tmem + kPCol + 64 * (jj & 1) + 8 * kk,
-                               mnmajor_sw128_desc(su32(S.V[s][0]) + kk * 2048, kSvHalf), (jj | kk) != 0);
-          umma_commit(&S.vempty[s]);      // V_jj consumed
-          umma_commit(&S.pvdone[jj & 1]); // O holds blocks 0..jj; P buffer jj % 2 free
+            for (int kk = 0; kk < 8; ++kk)
+              umma_f16_ts<kIdescPV>(tmem + 256, tmem + kPCol + 64 * (JJ & 1) + 8 * kk,
+                                    mnmajor_sw128_desc(su32(S.V[s][0]) + kk * 2048, kSvHalf), (jj | kk) != 0);
+            umma_commit(&S.vempty[s]);      // V_jj consumed
+            umma_commit(&S.pvdone[JJ & 1]); // O holds blocks 0..jj; P buffer JJ % 2 free
+          }
+          __syncwarp();
         }
-        __syncwarp();
       }
+      J0 += nblk;
     }
   } else {
     // ================= softmax: thread = query row r, key / channel columns [64·ch, 64·ch + 64)
@@ -166,15 +192,19 @@ calib_sv_tc_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_consta
     // the row sum are combined through shared memory, named barrier 1 + q)
     const int quarter = warp & 3, ch = warp >> 2;
     const int r = quarter * 32 + lane;
+    const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16);
+    const int cb = 64 * ch;                          // first column of this warp
+    int J0 = 0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    int q0, qh, kbeg, nblk;
+    item(it, q0, qh, kbeg, nblk);
     const int qi = q0 + r;
     const bool live = qi < p.N;
     const int lo = live ? sv_seq_start(p.starts, p.n_seq, qi) : 0x7fffffff;
-    const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16);
-    const int cb = 64 * ch;                          // first column of this warp
     float m = -INFINITY, l = 0.f;
     for (int j = 0; j < nblk; ++j) {
-      const int b = j & 1, key0 = kbeg + j * kSvK;
-      mbar_wait(&S.sfull[b], (j >> 1) & 1);
+      const int J = J0 + j, b = J & 1, key0 = kbeg + j * kSvK;
+      mbar_wait(&S.sfull[b], (J >> 1) & 1);
       fence_after();
       // keys key0 + c valid for this row: lo <= key <= qi
       const int cmin = lo - key0, cmax = live ? qi - key0 : -1;
@@ -204,9 +234,9 @@ calib_sv_tc_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_consta
       S.xmax[b][ch][r] = bm;
       asm volatile("bar.sync %0, 64;\n" ::"r"(1 + quarter) : "memory");
       bm = fmaxf(bm, S.xmax[b][ch ^ 1][r]);
-      // P buffer j % 2 free: P_{j-2}·V_{j-2} done
-      if (j >= 2) {
-        mbar_wait(&S.pvdone[j & 1], ((j >> 1) - 1) & 1);
+      // P buffer J % 2 free: P_{J-2}·V_{J-2} done (possibly the previous item's)
+      if (J >= 2) {
+        mbar_wait(&S.pvdone[J & 1], ((J >> 1) - 1) & 1);
         fence_after();
       }
       // (both warps of the row take the same decision; the TMEM load / store below are
@@ -220,7 +250,7 @@ calib_sv_tc_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_consta
       if (__any_sync(0xffffffffu, resc)) {
         // O holds blocks 0..j-1 once P_{j-1}·V_{j-1} is done (the MMAs complete in issue order)
         if (j >= 1) {
-          mbar_wait(&S.pvdone[(j - 1) & 1], ((j - 1) >> 1) & 1);
+          mbar_wait(&S.pvdone[(J - 1) & 1], ((J - 1) >> 1) & 1);
           fence_after();
         }
 #pragma unroll 1
@@ -262,21 +292,22 @@ calib_sv_tc_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_consta
           }
         }
         // keys c0 .. c0 + 31 -> TMEM columns kPCol + 64·(j % 2) + c0 / 2 .. + 15 of this lane
-        OSCAR_TMEM_ST16(trow + kPCol + 64 * (j & 1) + c0 / 2, pk);
+        OSCAR_TMEM_ST16(trow + kPCol + 64 * (J & 1) + c0 / 2, pk);
       }
       asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
       fence_before();
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(&S.sempty[b]);
-        mbar_arrive(&S.pfull[j & 1]);
+        mbar_arrive(&S.pfull[J & 1]);
       }
     }
     // row sum of both halves, then O / l -> SV bf16 [N][H_q][128] (this warp's 64 channels)
     S.xl[ch][r] = l;
     asm volatile("bar.sync %0, 64;\n" ::"r"(1 + quarter) : "memory");
     l += S.xl[ch ^ 1][r];
-    mbar_wait(&S.pvdone[(nblk - 1) & 1], ((nblk - 1) >> 1) & 1);
+    const int JL = J0 + nblk - 1;                     // this item's last block
+    mbar_wait(&S.pvdone[JL & 1], (JL >> 1) & 1);
     fence_after();
     const float inv = l > 0.f ? 1.f / l : 0.f;
     uint16_t* dst = p.SV + ((size_t)qi * p.hq + qh) * kD;
@@ -294,6 +325,12 @@ calib_sv_tc_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_consta
               pack_bf16x2(__uint_as_float(o[8 * q + 4]) * inv, __uint_as_float(o[8 * q + 5]) * inv),
               pack_bf16x2(__uint_as_float(o[8 * q + 6]) * inv, __uint_as_float(o[8 * q + 7]) * inv));
       }
+    }
+    // O read: the next item's first P·V may overwrite it
+    fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&S.oempty);
+    J0 += nblk;
     }
   }
   fence_before();
@@ -325,7 +362,9 @@ cudaError_t launch_calib_sv_tc(const oscar_ctx& c, const void* Q, const void* K,
   const int smem = (int)sizeof(SvSmem) + 1024;
   cudaError_t e = cudaFuncSetAttribute(calib_sv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  calib_sv_tc_kernel<<<dim3((unsigned)p.nqb, (unsigned)c.hq), kSvThreads, smem, s>>>(mq, mk, mv, p);
+  const long items = (long)p.nqb * c.hq;
+  const int grid = (int)(items < c.num_sms ? items : c.num_sms);   // persistent: one CTA per SM
+  calib_sv_tc_kernel<<<grid, kSvThreads, smem, s>>>(mq, mk, mv, p);
   return cudaGetLastError();
 }
 

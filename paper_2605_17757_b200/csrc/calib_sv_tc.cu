@@ -34,7 +34,10 @@ constexpr int kSvHalf = 128 * 128;            // one 64-channel (or 64-key) half
 constexpr int kSvThreads = 10 * 32;
 constexpr int kSvStages = 3;                  // K ring (a stage frees once its Q·Kᵀ completes)
 constexpr int kSvVStages = 2;                 // V ring (a stage frees once its P·V completes)
-constexpr float kRescaleThr = 8.f;            // log2 units
+#ifndef OSCAR_SV_RESCALE_THR
+#define OSCAR_SV_RESCALE_THR 8.f
+#endif
+constexpr float kRescaleThr = OSCAR_SV_RESCALE_THR;   // log2 units
 
 struct SvSmem {
   alignas(1024) uint8_t Q[2][kSvHalf];        // [channel half][query row][128 B]

@@ -113,10 +113,11 @@ __device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
   return r;
 }
 
-// packed f32x2 epilogue arithmetic: same-box A/B, C2 prefill 2-bit G = 64 0.560 (scalar) vs
-// 0.577 ms (f32x2), 3-bit 0.658 vs 0.647 ms -> on for 3-bit codes only
+// packed f32x2 epilogue arithmetic, same-box A/B at the C2 prefill shape (scalar vs f32x2, ms):
+// 2-bit G = 64 0.557 vs 0.573; G = 32 0.604 vs 0.592; G = 128 0.619 vs 0.594; 3-bit G = 64 0.658 vs
+// 0.647; 4-bit G = 64 0.626 vs 0.623; G = 32 0.647 vs 0.625 -> on except for 2-bit G = 64
 #ifndef OSCAR_APPEND_F2
-#define OSCAR_APPEND_F2 (BITS == 3)
+#define OSCAR_APPEND_F2 (!(BITS == 2 && G == 64))
 #endif
 #ifndef OSCAR_APPEND_F2ADD
 #define OSCAR_APPEND_F2ADD OSCAR_APPEND_F2     // the x·R_hi + x·R_lo sum alone as f32x2
